@@ -1,0 +1,59 @@
+"""The five BASELINE.json configs as data (nets, batch, partitions, hparams).
+
+PPVs: paper values where the paper gives them (Table 1 PAPER.md L91-98,
+Table 5), otherwise the roofline-balanced block-boundary PPVs of
+SURVEY.md Appendix A.  Hyperparameters: Appendix A/B of the paper
+(PAPER.md L282-306): momentum 0.9; weight decay 5e-4 (LeNet, VGG), 4e-3
+(AlexNet), 1e-4 (ResNet); base lr 0.01 (LeNet), 0.001 (AlexNet), 0.1 (VGG,
+ResNet); the pipelined ResNet's stale stages use the Table 7 BKS_2 rate
+(0.001 for ResNet-110/362), the last stage the base rate (reading AMB-9).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, Tuple
+
+from .nets import NetSpec, by_name
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    net: str
+    batch: int
+    ppv: Dict[int, Tuple[int, ...]]       # K -> PPV (K-1 weighted-layer numbers)
+    base_lr: float
+    stale_lr: float                         # lr of every non-last stage when K > 1
+    momentum: float
+    weight_decay: float
+    steps: int
+    milestones: Tuple[int, ...] = ()
+    gamma: float = 0.1
+    steps_per_epoch: int = 390
+    hybrid_epoch: int = -1
+
+    def netspec(self) -> NetSpec:
+        return by_name(self.net)
+
+    def lr_vector(self, K: int):
+        if K == 1:
+            return [self.base_lr]
+        return [self.stale_lr] * (K - 1) + [self.base_lr]
+
+
+CONFIGS = {
+    "lenet5": Config("lenet5", "lenet5", 64, {1: (), 2: (1,), 3: (1, 2), 4: (1, 2, 3)},
+                     0.01, 0.01, 0.9, 5e-4, 20),
+    "alexnet": Config("alexnet", "alexnet", 128, {1: (), 2: (1,), 4: (1, 2, 3)},
+                      0.001, 0.001, 0.9, 4e-3, 100),
+    "vgg16": Config("vgg16", "vgg16", 128,
+                    {1: (), 2: (2,), 4: (2, 4, 7), 8: (1, 2, 4, 6, 7, 9, 10)},
+                    0.1, 0.1, 0.9, 5e-4, 100),
+    "resnet110": Config("resnet110", "resnet110", 128,
+                        {1: (), 2: (37,), 4: (17, 33, 61), 8: (9, 17, 25, 33, 45, 61, 81)},
+                        0.1, 0.001, 0.9, 1e-4, 100, milestones=(100, 150)),
+    "resnet362": Config("resnet362", "resnet362", 128,
+                        {1: (), 2: (121,), 8: (27, 55, 81, 107, 147, 201, 265)},
+                        0.1, 0.001, 0.9, 1e-4, 20, milestones=(100, 150),
+                        steps_per_epoch=5, hybrid_epoch=2),
+}
