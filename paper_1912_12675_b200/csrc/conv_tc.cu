@@ -1,0 +1,693 @@
+// conv_tc.cu -- implicit-GEMM convolution on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// Forward (x^(l) from x^(l-1) and W^(l)) and dgrad (L47: delta^(l-1)
+// from delta^(l) with the CURRENT weights, reading AMB-2) are one kernel:
+//   D[p, co] = sum_tap sum_ci  X[n, y*S + off + sgn*r, x*S + off + sgn*s, ci] * Wt[tap][co][ci]
+// M = 128 output pixels (an (img, y, x) box), N = output channels, K = taps x
+// input channels.  Each K step loads, with one TMA per 16-byte channel chunk, the
+// shifted 128-pixel box of the input (zero fill outside the image = the
+// convolution's zero padding) and the tap's weight slice.
+//
+// Weight gradient (L47: de/dW^(l) from x^(l-1) and delta^(l)):
+//   D[tap*Cinp + ci, co] = sum_p X_shift(tap)[p, ci] * dY[p, co]
+// M = (tap, ci) rows from shifted input boxes (MN-major operand), N = co
+// (MN-major), K = output pixels split over CTAs; partial sums are reduced by the
+// SGD kernel.
+//
+// Precision (common.h): in the default build operands are float32 in smem and
+// every product is 3xTF32 -- D += Ahi*Bhi + Ahi*Blo + Alo*Bhi, where the tensor
+// core truncates float32 to tf32 (= hi) and lo = v - trunc(v) comes from a
+// converter warpgroup (activations) or from a precomputed shadow (weights).
+//
+// Structure: persistent CTAs, warp-specialised: warp 0 TMA producer, warp 1 MMA
+// issuer (+TMEM allocator), warps 2..5 epilogue, warps 6..9 split converter
+// (3xTF32 build only).  smem ring of `stages` slots (full / ready / empty
+// mbarriers), double-buffered TMEM accumulators (tmem_full / tmem_empty).
+#include "kernels.h"
+#include "ptx.cuh"
+
+#include <algorithm>
+
+namespace pst {
+
+namespace {
+
+constexpr int kBaseThreads = 192;
+constexpr int kThreads = kBaseThreads + (PST_SPLIT ? 128 : 0);
+constexpr int kEpiThreads = 128;
+constexpr int kMaxStages = 8;
+constexpr int kMmaK = 32 / (int)sizeof(act_t);   // K elements per MMA instruction (2 chunks)
+
+struct FwdArgs {
+  int N, Ho, Wo;
+  int bimg, bh, bw, tn, ty, tx;
+  int n_mtiles, n_ntiles, n_tiles;
+  int Cinp, kc, n_kc, k, taps, S, off, sgn;
+  int Coutp, BN, Cout;
+  int stages;
+  uint32_t a_bytes, b_bytes, stage_bytes, tx_bytes;
+  uint32_t tmem_cols;
+  int epi, relu;
+  void* out;
+  const float* bias;
+  double* stats;
+  const act_t* res;
+  int res_mode, res_H, res_W, res_C, res_pad;
+};
+
+__device__ __forceinline__ void decode_tile_px(const FwdArgs& a, int mt, int row, int& n, int& y,
+                                               int& x) {
+  const int ix = mt % a.tx;
+  const int iy = (mt / a.tx) % a.ty;
+  const int it = mt / (a.tx * a.ty);
+  const int xb = row % a.bw;
+  const int yb = (row / a.bw) % a.bh;
+  const int nb = row / (a.bw * a.bh);
+  n = it * a.bimg + nb;
+  y = iy * a.bh + yb;
+  x = ix * a.bw + xb;
+}
+
+// 3xTF32 split: lo[i] = raw[i] - trunc_tf32(raw[i]) over `nbytes` of smem, by 128 threads.
+__device__ __forceinline__ void split_lo(const uint8_t* raw, uint8_t* lo, uint32_t nbytes, int t) {
+  const float4* r = reinterpret_cast<const float4*>(raw);
+  float4* l = reinterpret_cast<float4*>(lo);
+  for (uint32_t i = t; i < nbytes / 16; i += 128) {
+    float4 v = r[i];
+    l[i] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+  }
+}
+
+__device__ __forceinline__ void store16(void* dst, const float* v) {
+#if PST_SPLIT
+  float4* op = reinterpret_cast<float4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+#else
+  alignas(16) act_t h[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) h[i] = f2act(v[i]);
+  uint4* op = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < (int)(16 * sizeof(act_t) / 16); ++i) op[i] = reinterpret_cast<uint4*>(h)[i];
+#endif
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmBlo, const FwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // [stages x stage_bytes] [sbuf 16x129 f32] [acc doubles 2*Coutp] [barriers] [tmem ptr]
+  // stage: [A raw][B raw]([A lo][B lo] in the split build)
+  uint8_t* ring = smem;
+  float* sbuf = reinterpret_cast<float*>(smem + a.stages * a.stage_bytes);
+  double* cacc = reinterpret_cast<double*>(sbuf + 16 * 129 + 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cacc + 2 * a.Coutp);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kMaxStages;
+  uint64_t* ready = bars + 2 * kMaxStages;
+  uint64_t* tfull = bars + 3 * kMaxStages;
+  uint64_t* tempty = bars + 3 * kMaxStages + 2;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.stages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+      ptx::mbar_init(&ready[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (a.epi == EPI_BN_STATS)
+    for (int i = threadIdx.x; i < 2 * a.Coutp; i += blockDim.x) cacc[i] = 0.0;
+  if (warp == 1) ptx::tmem_alloc(tmem_ptr, a.tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr;
+  const int nch = a.kc / kEPC;   // 16-byte channel chunks per stage
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tmA);
+      ptx::prefetch_tmap(&tmB);
+      if (PST_SPLIT) ptx::prefetch_tmap(&tmBlo);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+        const int mt = t / a.n_ntiles, nt = t % a.n_ntiles;
+        const int ix = mt % a.tx, iy = (mt / a.tx) % a.ty, it = mt / (a.tx * a.ty);
+        const int x0 = ix * a.bw * a.S + a.off, y0 = iy * a.bh * a.S + a.off, n0 = it * a.bimg;
+        for (int tap = 0; tap < a.taps; ++tap) {
+          const int r = tap / a.k, s = tap % a.k;
+          for (int kcc = 0; kcc < a.n_kc; ++kcc) {
+            ptx::mbar_wait(&empty[st], ph ^ 1);
+            ptx::mbar_expect_tx(&full[st], a.tx_bytes);
+            uint8_t* sa = ring + st * a.stage_bytes;
+            uint8_t* sb = sa + a.a_bytes;
+            for (int j = 0; j < nch; ++j) {
+              const int cc = kcc * nch + j;
+              ptx::tma_load_5d(sa + j * 2048, &tmA, &full[st], 0, cc, x0 + a.sgn * s, y0 + a.sgn * r, n0);
+              ptx::tma_load_4d(sb + j * (a.BN * 16), &tmB, &full[st], 0, cc, nt * a.BN, tap);
+#if PST_SPLIT
+              ptx::tma_load_4d(sb + a.a_bytes + a.b_bytes + j * (a.BN * 16), &tmBlo, &full[st], 0, cc,
+                               nt * a.BN, tap);
+#endif
+            }
+            if (++st == a.stages) { st = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_mma(128, a.BN, 0, 0, PST_AB_FORMAT);
+      int st = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t use = (uint32_t)(local >> 1);
+        ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t dtm = tmem_base + acc * a.BN;
+        int kiter = 0;
+        for (int tap = 0; tap < a.taps; ++tap) {
+          for (int kcc = 0; kcc < a.n_kc; ++kcc, ++kiter) {
+            ptx::mbar_wait(PST_SPLIT ? &ready[st] : &full[st], ph);
+            ptx::tc_fence_after();
+            const uint32_t sa = ptx::smem_u32(ring + st * a.stage_bytes);
+            const uint32_t sb = sa + a.a_bytes;
+            for (int kk = 0; kk < nch / 2; ++kk) {
+              const uint64_t ad = ptx::smem_desc(sa + kk * 2 * 2048, 2048, 128);
+              const uint64_t bd = ptx::smem_desc(sb + kk * 2 * (a.BN * 16), a.BN * 16, 128);
+              const uint32_t accum = (kiter > 0 || kk > 0) ? 1u : 0u;
+              ptx::umma(dtm, ad, bd, idesc, accum);
+#if PST_SPLIT
+              const uint32_t off_lo = a.a_bytes + a.b_bytes;
+              const uint64_t adl = ptx::smem_desc(sa + off_lo + kk * 2 * 2048, 2048, 128);
+              const uint64_t bdl = ptx::smem_desc(sb + off_lo + kk * 2 * (a.BN * 16), a.BN * 16, 128);
+              ptx::umma(dtm, ad, bdl, idesc, 1u);
+              ptx::umma(dtm, adl, bd, idesc, 1u);
+#endif
+            }
+            ptx::umma_commit(&empty[st]);
+            if (++st == a.stages) { st = 0; ph ^= 1; }
+          }
+        }
+        ptx::umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;            // TMEM lane quarter accessible by this warp
+    const int row = q * 32 + lane;     // pixel row within the tile
+    const int et = threadIdx.x - 64;   // 0..127
+    int local = 0;
+    for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++local) {
+      const int mt = t / a.n_ntiles, nt = t % a.n_ntiles;
+      const int acc = local & 1;
+      const uint32_t use = (uint32_t)(local >> 1);
+      ptx::mbar_wait(&tfull[acc], use & 1);
+      ptx::tc_fence_after();
+      int n, y, x;
+      decode_tile_px(a, mt, row, n, y, x);
+      const bool valid = (n < a.N) && (y < a.Ho) && (x < a.Wo);
+      const int64_t pix = ((int64_t)n * a.Ho + y) * a.Wo + x;
+      for (int ch = 0; ch < a.BN / 16; ++ch) {
+        float v[16];
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * a.BN + ch * 16;
+        ptx::tmem_ld16(taddr, v);
+        if (ch == a.BN / 16 - 1) {
+          ptx::tc_fence_before();
+          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        }
+        const int c0 = nt * a.BN + ch * 16;
+        if (a.epi == EPI_BN_STATS) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = valid ? act2f(f2act(v[i])) : 0.f;
+        } else if (a.epi == EPI_BIAS_ACT || a.epi == EPI_BIAS_F32) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int c = c0 + i;
+            const float b = (a.bias != nullptr && c < a.Cout) ? __ldg(&a.bias[c]) : 0.f;
+            float o = v[i] + b;
+            if (a.relu) o = fmaxf(o, 0.f);
+            v[i] = (c < a.Cout) ? o : 0.f;
+          }
+        } else {  // EPI_DGRAD: + shortcut^T of the residual layer's gradient
+          if (valid && a.res_mode == 1) {
+            const act_t* rp = a.res + pix * a.Coutp + c0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += act2f(rp[i]);
+          } else if (valid && a.res_mode == 2 && ((y | x) & 1) == 0) {
+            const int64_t rpix = ((int64_t)n * a.res_H + (y >> 1)) * a.res_W + (x >> 1);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int c = c0 + i;
+              if (c < a.Cout) v[i] += act2f(a.res[rpix * a.res_C + c + a.res_pad]);
+            }
+          }
+        }
+        if (valid) {
+          if (a.epi == EPI_BIAS_F32) {
+            float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + pix * a.Coutp + c0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else {
+            store16(reinterpret_cast<act_t*>(a.out) + pix * a.Coutp + c0, v);
+          }
+        }
+        if (a.epi == EPI_BN_STATS) {
+          // per-channel sums over the 128 pixel rows via an smem transpose
+#pragma unroll
+          for (int i = 0; i < 16; ++i) sbuf[i * 129 + row] = v[i];
+          ptx::named_bar_sync(1, kEpiThreads);
+          const int c = et >> 3, part = et & 7;
+          float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float u = sbuf[c * 129 + part * 16 + j];
+            s1 += u;
+            s2 += u * u;
+          }
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) {
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+          }
+          if (part == 0) {
+            cacc[2 * (c0 + c)] += (double)s1;
+            cacc[2 * (c0 + c) + 1] += (double)s2;
+          }
+          ptx::named_bar_sync(1, kEpiThreads);
+        }
+      }
+    }
+    if (a.epi == EPI_BN_STATS) {
+      ptx::named_bar_sync(1, kEpiThreads);
+      for (int i = et; i < 2 * a.Coutp; i += kEpiThreads)
+        if (cacc[i] != 0.0) atomicAdd(&a.stats[i], cacc[i]);
+    }
+  } else {
+#if PST_SPLIT
+    // ------------------------------------------------------------ 3xTF32 split converter (warps 6..9)
+    const int ct = threadIdx.x - kBaseThreads;   // 0..127
+    int st = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+      for (int kit = 0; kit < a.taps * a.n_kc; ++kit) {
+        ptx::mbar_wait(&full[st], ph);
+        uint8_t* sa = ring + st * a.stage_bytes;
+        split_lo(sa, sa + a.a_bytes + a.b_bytes, a.a_bytes, ct);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&ready[st]);
+        if (++st == a.stages) { st = 0; ph ^= 1; }
+      }
+    }
+#endif
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, a.tmem_cols);
+  }
+}
+
+// ---------------------------------------------------------------- weight gradient
+// pixels per K stage.  The 3xTF32 build stages 32 pixels: kind::tf32 needs
+// K-major operands, so the converter transposes each [pixel][4 ch] chunk into
+// K-major core matrices (8 rows x 4 pixels) in place while it splits hi/lo.
+constexpr int kWgPix = PST_SPLIT ? 32 : 64;
+constexpr int kWgSbo = (kWgPix / 4) * 128;   // split build: byte stride between 8-row groups
+constexpr int kWgUnitsPerThread = 6;         // split build: 4x4 transpose blocks per converter thread
+
+// split build: raw MN-major [chunk][px][4 ch] -> K-major hi (in place) and lo planes
+__device__ __forceinline__ void split_transpose(uint8_t* base, uint8_t* lo_base, int nchunks, int ct) {
+  const int units = nchunks * (kWgPix / 4);
+  float4 v[kWgUnitsPerThread][4];
+#pragma unroll
+  for (int i = 0; i < kWgUnitsPerThread; ++i) {
+    const int u = ct + i * 128;
+    if (u < units) {
+      const int q = u / (kWgPix / 4), pq = u % (kWgPix / 4);
+      const float4* src = reinterpret_cast<const float4*>(base + (q * kWgPix + 4 * pq) * 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[i][k] = src[k];
+    }
+  }
+  ptx::named_bar_sync(2, 128);
+#pragma unroll
+  for (int i = 0; i < kWgUnitsPerThread; ++i) {
+    const int u = ct + i * 128;
+    if (u < units) {
+      const int q = u / (kWgPix / 4), pq = u % (kWgPix / 4);
+      const float* f = reinterpret_cast<const float*>(v[i]);   // f[px*4 + ch]
+#pragma unroll
+      for (int cl = 0; cl < 4; ++cl) {
+        const int r = 4 * q + cl;
+        const uint32_t off = (uint32_t)((r >> 3) * kWgSbo + pq * 128 + (r & 7) * 16);
+        const float4 hi = make_float4(f[cl], f[4 + cl], f[8 + cl], f[12 + cl]);
+        *reinterpret_cast<float4*>(base + off) = hi;
+        *reinterpret_cast<float4*>(lo_base + off) =
+            make_float4(tf32_lo(hi.x), tf32_lo(hi.y), tf32_lo(hi.z), tf32_lo(hi.w));
+      }
+    }
+  }
+}
+
+struct WgArgs {
+  int N, Ho, Wo;
+  int bimg, bh, bw, tn, ty, tx, n_ptiles;
+  int Cinp, Coutp, BNw, n_ntiles, k, taps, S, pad;
+  int rows, n_mt, G, n_mgroups, ksplit;
+  int stages;
+  uint32_t x_bytes, d_bytes, stage_bytes;
+  uint32_t tmem_cols;
+  float* part;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_wgrad_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD,
+                      const WgArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // stage: [X raw (x_bytes)][dY raw (d_bytes)]([X lo][dY lo] in the split build)
+  uint8_t* ring = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.stages * a.stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kMaxStages;
+  uint64_t* ready = bars + 2 * kMaxStages;
+  uint64_t* tfull = bars + 3 * kMaxStages;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int b = blockIdx.x;
+  const int mg = b % a.n_mgroups;
+  const int nt = (b / a.n_mgroups) % a.n_ntiles;
+  const int ks = b / (a.n_mgroups * a.n_ntiles);
+  const int p_lo = (int)((int64_t)ks * a.n_ptiles / a.ksplit);
+  const int p_hi = (int)((int64_t)(ks + 1) * a.n_ptiles / a.ksplit);
+  const int mt0 = mg * a.G;
+  const int g_cnt = min(a.G, a.n_mt - mt0);
+  const int r0 = mt0 * 128;
+  const int r_end = min(r0 + g_cnt * 128, a.rows);
+  const int q0 = r0 / kEPC, q1 = (r_end + kEPC - 1) / kEPC;   // global row chunks loaded: [q0, q1)
+  const int cin_c = a.Cinp / kEPC, bn_c = a.BNw / kEPC;
+  const uint32_t used_x = (uint32_t)(q1 - q0) * (kWgPix * 16);
+  const uint32_t used_d = (uint32_t)bn_c * (kWgPix * 16);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.stages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+      ptx::mbar_init(&ready[i], 4);
+    }
+    ptx::mbar_init(&tfull[0], 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_ptr, a.tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr;
+  const int n_iter = p_hi - p_lo;
+
+  if (warp == 0) {
+    if (lane == 0 && n_iter > 0) {
+      ptx::prefetch_tmap(&tmX);
+      ptx::prefetch_tmap(&tmD);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int pt = p_lo; pt < p_hi; ++pt) {
+        const int ix = pt % a.tx, iy = (pt / a.tx) % a.ty, it = pt / (a.tx * a.ty);
+        const int xo = ix * a.bw, yo = iy * a.bh, n0 = it * a.bimg;
+        ptx::mbar_wait(&empty[st], ph ^ 1);
+        ptx::mbar_expect_tx(&full[st], used_x + used_d);
+        uint8_t* sx = ring + st * a.stage_bytes;
+        uint8_t* sd = sx + a.x_bytes;
+        for (int j = 0; j < bn_c; ++j)
+          ptx::tma_load_5d(sd + j * (kWgPix * 16), &tmD, &full[st], 0, nt * bn_c + j, xo, yo, n0);
+        for (int qq = q0; qq < q1; ++qq) {
+          const int tap = qq / cin_c, cc = qq % cin_c;
+          const int r = tap / a.k, s = tap % a.k;
+          ptx::tma_load_5d(sx + (qq - q0) * (kWgPix * 16), &tmX, &full[st], 0, cc, xo * a.S - a.pad + s,
+                           yo * a.S - a.pad + r, n0);
+        }
+        if (++st == a.stages) { st = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_iter > 0) {
+#if PST_SPLIT
+      const uint32_t idesc = ptx::idesc_mma(128, a.BNw, 0, 0, PST_AB_FORMAT);   // K-major (converted)
+#else
+      const uint32_t idesc = ptx::idesc_mma(128, a.BNw, 1, 1, PST_AB_FORMAT);   // MN-major (as loaded)
+#endif
+      const uint32_t mtile_bytes = 128 * kWgPix * (uint32_t)sizeof(act_t);   // one 128-row M tile
+      int st = 0;
+      uint32_t ph = 0;
+      for (int it = 0; it < n_iter; ++it) {
+        ptx::mbar_wait(PST_SPLIT ? &ready[st] : &full[st], ph);
+        ptx::tc_fence_after();
+        const uint32_t sx = ptx::smem_u32(ring + st * a.stage_bytes);
+        const uint32_t sd = sx + a.x_bytes;
+        for (int j = 0; j < g_cnt; ++j) {
+          const uint32_t abase = sx + (uint32_t)j * mtile_bytes;
+          const uint32_t dt = tmem_base + j * a.BNw;
+          for (int kk = 0; kk < kWgPix / kMmaK; ++kk) {
+#if PST_SPLIT
+            // K-major: core matrix = 8 rows x 4 pixels (128 B); LBO 128 (next 4 px), SBO = 8-row group
+            const uint32_t lo = a.x_bytes + a.d_bytes;
+            const uint64_t ad = ptx::smem_desc(abase + kk * 256, 128, kWgSbo);
+            const uint64_t bd = ptx::smem_desc(sd + kk * 256, 128, kWgSbo);
+            const uint64_t adl = ptx::smem_desc(abase + lo + kk * 256, 128, kWgSbo);
+            const uint64_t bdl = ptx::smem_desc(sd + lo + kk * 256, 128, kWgSbo);
+            ptx::umma(dt, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+            ptx::umma(dt, ad, bdl, idesc, 1u);
+            ptx::umma(dt, adl, bd, idesc, 1u);
+#else
+            const uint64_t ad = ptx::smem_desc(abase + kk * kMmaK * 16, 128, kWgPix * 16);
+            const uint64_t bd = ptx::smem_desc(sd + kk * kMmaK * 16, 128, kWgPix * 16);
+            ptx::umma(dt, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+#endif
+          }
+        }
+        ptx::umma_commit(&empty[st]);
+        if (++st == a.stages) { st = 0; ph ^= 1; }
+      }
+      ptx::umma_commit(&tfull[0]);
+    }
+  } else if (warp < 6) {
+    const int q = warp & 3;
+    const int rowl = q * 32 + lane;
+    if (n_iter > 0) {
+      ptx::mbar_wait(&tfull[0], 0);
+      ptx::tc_fence_after();
+    }
+    for (int j = 0; j < g_cnt; ++j) {
+      const int rg = r0 + j * 128 + rowl;
+      for (int ch = 0; ch < a.BNw / 16; ++ch) {
+        float v[16];
+        if (n_iter > 0) {
+          ptx::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + j * a.BNw + ch * 16, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (rg < a.rows) {
+          float4* op = reinterpret_cast<float4*>(a.part + ((int64_t)ks * a.rows + rg) * a.Coutp +
+                                                 nt * a.BNw + ch * 16);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+    }
+  } else {
+#if PST_SPLIT
+    const int ct = threadIdx.x - kBaseThreads;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int it = 0; it < n_iter; ++it) {
+      ptx::mbar_wait(&full[st], ph);
+      uint8_t* sx = ring + st * a.stage_bytes;
+      const uint32_t lo = a.x_bytes + a.d_bytes;
+      split_transpose(sx, sx + lo, q1 - q0, ct);
+      split_transpose(sx + a.x_bytes, sx + a.x_bytes + lo, bn_c, ct);
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&ready[st]);
+      if (++st == a.stages) { st = 0; ph ^= 1; }
+    }
+#endif
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, a.tmem_cols);
+  }
+}
+
+// largest multiple of 16 that divides C and is <= cap (C a multiple of 16)
+int tile_n(int C, int cap) {
+  int best = 16;
+  for (int b = 16; b <= cap && b <= C; b += 16)
+    if (C % b == 0) best = b;
+  return best;
+}
+
+int pow2_at_least(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+void pixel_tile(int N, int Ho, int Wo, int npx, int& bimg, int& bh, int& bw) {
+  (void)N;
+  bw = std::min(pow2_at_least(Wo), npx);
+  bh = std::min(pow2_at_least(Ho), npx / bw);
+  bimg = npx / (bw * bh);
+}
+
+// activation tensor map: dims (EPC, Cp/EPC, W, H, N), box (EPC, 1, bw*S, bh*S, bimg)
+CUtensorMap act_tmap(const act_t* p, int N, int H, int W, int Cp, int bimg, int bh, int bw, int S) {
+  const uint64_t es = sizeof(act_t);
+  uint64_t dims[5] = {(uint64_t)kEPC, (uint64_t)Cp / kEPC, (uint64_t)W, (uint64_t)H, (uint64_t)N};
+  uint64_t str[4] = {16, (uint64_t)Cp * es, (uint64_t)W * Cp * es, (uint64_t)H * W * Cp * es};
+  uint32_t box[5] = {(uint32_t)kEPC, 1, (uint32_t)(bw * S), (uint32_t)(bh * S), (uint32_t)bimg};
+  uint32_t est[5] = {1, 1, (uint32_t)S, (uint32_t)S, 1};
+  return make_tmap(act_tmap_dtype(), 5, p, dims, str, box, est);
+}
+
+// weight shadow map: dims (EPC, Cinp/EPC, Coutp, taps), box (EPC, 1, BN, 1)
+CUtensorMap w_tmap(const act_t* p, int taps, int Coutp, int Cinp, int BN) {
+  const uint64_t es = sizeof(act_t);
+  uint64_t wd[4] = {(uint64_t)kEPC, (uint64_t)Cinp / kEPC, (uint64_t)Coutp, (uint64_t)taps};
+  uint64_t ws[3] = {16, (uint64_t)Cinp * es, (uint64_t)Coutp * Cinp * es};
+  uint32_t wb[4] = {(uint32_t)kEPC, 1, (uint32_t)BN, 1};
+  return make_tmap(act_tmap_dtype(), 4, p, wd, ws, wb, nullptr);
+}
+
+int choose_wg_G(int n_mt, int BNw) {
+  int G = std::max(1, std::min(n_mt, 512 / BNw));
+  const int lo = PST_SPLIT ? 2 : 1;
+  while (G > 1 && lo * (G * (128 / kEPC) + BNw / kEPC) * (kWgPix * 16) > 96 * 1024) --G;
+  // split build: each converter thread transposes at most kWgUnitsPerThread 4x4 blocks
+  while (PST_SPLIT && G > 1 && (G * (128 / kEPC) + BNw / kEPC) * (kWgPix / 4) > 128 * kWgUnitsPerThread) --G;
+  return G;
+}
+
+}  // namespace
+
+void conv_tc(const ConvSpec& c, cudaStream_t st) {
+  PST_CHECK_ARG(c.Cinp % 16 == 0 && c.Coutp % 16 == 0, "conv channels must be padded to 16");
+  PST_CHECK_ARG(c.S == 1 || c.S == 2, "conv stride must be 1 or 2");
+  PST_CHECK_ARG((reinterpret_cast<uintptr_t>(c.in) & 15) == 0, "conv input must be 16B aligned");
+  FwdArgs a{};
+  a.N = c.N; a.Ho = c.Ho; a.Wo = c.Wo;
+  pixel_tile(c.N, c.Ho, c.Wo, 128, a.bimg, a.bh, a.bw);
+  a.tn = ceil_div(c.N, a.bimg); a.ty = ceil_div(c.Ho, a.bh); a.tx = ceil_div(c.Wo, a.bw);
+  a.n_mtiles = a.tn * a.ty * a.tx;
+  a.BN = tile_n(c.Coutp, 256);
+  a.n_ntiles = c.Coutp / a.BN;
+  a.n_tiles = a.n_mtiles * a.n_ntiles;
+  a.Cinp = c.Cinp;
+  // channels per K stage: <= 128 bytes per pixel, a multiple of one MMA's K (2 chunks)
+  const int kc_max = 128 / (int)sizeof(act_t);
+  a.kc = 2 * kEPC;
+  for (int kc = 2 * kEPC; kc <= kc_max; kc += 2 * kEPC)
+    if (c.Cinp % kc == 0) a.kc = kc;
+  a.n_kc = c.Cinp / a.kc;
+  a.k = c.k; a.taps = c.k * c.k; a.S = c.S; a.off = c.off; a.sgn = c.sgn;
+  a.Coutp = c.Coutp; a.Cout = c.Cout;
+  const int nch = a.kc / kEPC;
+  a.a_bytes = (uint32_t)nch * 2048;
+  a.b_bytes = (uint32_t)nch * a.BN * 16;
+  a.tx_bytes = a.a_bytes + a.b_bytes * (PST_SPLIT ? 2 : 1);
+  a.stage_bytes = (a.a_bytes + a.b_bytes) * (PST_SPLIT ? 2 : 1);
+  const int budget = 190 * 1024;
+  a.stages = std::max(2, std::min(kMaxStages, budget / (int)a.stage_bytes));
+  a.tmem_cols = (uint32_t)std::max(32, pow2_at_least(2 * a.BN));
+  a.epi = c.epi; a.relu = c.relu; a.out = c.out; a.bias = c.bias; a.stats = c.stats;
+  a.res = c.res; a.res_mode = c.res_mode; a.res_H = c.res_H; a.res_W = c.res_W; a.res_C = c.res_C;
+  a.res_pad = c.res_pad;
+
+  CUtensorMap tA = act_tmap(c.in, c.N, c.H, c.W, c.Cinp, a.bimg, a.bh, a.bw, c.S);
+  CUtensorMap tB = w_tmap(c.wshadow, a.taps, c.Coutp, c.Cinp, a.BN);
+  CUtensorMap tBlo = PST_SPLIT ? w_tmap(c.wshadow + (size_t)a.taps * c.Coutp * c.Cinp, a.taps, c.Coutp, c.Cinp, a.BN)
+                               : tB;
+  const size_t smem = (size_t)a.stages * a.stage_bytes + (16 * 129 + 4) * 4 + 2 * c.Coutp * 8 +
+                      (3 * kMaxStages + 4) * 8 + 16;
+  PST_CHECK_ARG(smem <= 227 * 1024, "conv smem budget");
+  PST_CUDA(cudaFuncSetAttribute(conv_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev;
+  PST_CUDA(cudaGetDevice(&dev));
+  const int grid = std::min(a.n_tiles, num_sms(dev));
+  conv_fwd_kernel<<<grid, kThreads, smem, st>>>(tA, tB, tBlo, a);
+  PST_CUDA(cudaGetLastError());
+}
+
+WgradPlan wgrad_plan(int N, int Ho, int Wo, int Cinp, int Coutp, int k, int num_sm) {
+  int bimg, bh, bw;
+  pixel_tile(N, Ho, Wo, kWgPix, bimg, bh, bw);
+  const int n_ptiles = ceil_div(N, bimg) * ceil_div(Ho, bh) * ceil_div(Wo, bw);
+  const int rows = k * k * Cinp;
+  const int n_mt = ceil_div(rows, 128);
+  const int BNw = tile_n(Coutp, 256);
+  const int n_nt = Coutp / BNw;
+  const int G = choose_wg_G(n_mt, BNw);
+  const int n_mg = ceil_div(n_mt, G);
+  const int base = n_mg * n_nt;
+  int ksplit = std::max(1, std::min(n_ptiles, (2 * num_sm) / base));
+  ksplit = std::min(ksplit, std::max(1, n_ptiles / 2));
+  WgradPlan p;
+  p.ksplit = ksplit;
+  p.part_floats = (int64_t)ksplit * rows * Coutp;
+  return p;
+}
+
+void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
+  PST_CHECK_ARG(w.Cinp % 16 == 0 && w.Coutp % 16 == 0, "wgrad channels must be padded to 16");
+  WgArgs a{};
+  a.N = w.N; a.Ho = w.Ho; a.Wo = w.Wo;
+  pixel_tile(w.N, w.Ho, w.Wo, kWgPix, a.bimg, a.bh, a.bw);
+  a.tn = ceil_div(w.N, a.bimg); a.ty = ceil_div(w.Ho, a.bh); a.tx = ceil_div(w.Wo, a.bw);
+  a.n_ptiles = a.tn * a.ty * a.tx;
+  a.Cinp = w.Cinp; a.Coutp = w.Coutp;
+  a.BNw = tile_n(w.Coutp, 256);
+  a.n_ntiles = w.Coutp / a.BNw;
+  a.k = w.k; a.taps = w.k * w.k; a.S = w.S; a.pad = w.pad;
+  a.rows = a.taps * w.Cinp;
+  a.n_mt = ceil_div(a.rows, 128);
+  a.G = choose_wg_G(a.n_mt, a.BNw);
+  a.n_mgroups = ceil_div(a.n_mt, a.G);
+  a.ksplit = w.ksplit;
+  a.x_bytes = (uint32_t)a.G * (128 / kEPC) * (kWgPix * 16);
+  a.d_bytes = (uint32_t)(a.BNw / kEPC) * (kWgPix * 16);
+  a.stage_bytes = (a.x_bytes + a.d_bytes) * (PST_SPLIT ? 2 : 1);
+  a.stages = std::max(1, std::min(4, (200 * 1024) / (int)a.stage_bytes));
+  const size_t smem = (size_t)a.stages * a.stage_bytes + (3 * kMaxStages + 2) * 8 + 16;
+  PST_CHECK_ARG(smem <= 227 * 1024, "wgrad smem budget");
+  a.tmem_cols = (uint32_t)std::max(32, pow2_at_least(a.G * a.BNw));
+  a.part = w.part;
+
+  CUtensorMap tX = act_tmap(w.x, w.N, w.H, w.W, w.Cinp, a.bimg, a.bh, a.bw, w.S);
+  CUtensorMap tD = act_tmap(w.dy, w.N, w.Ho, w.Wo, w.Coutp, a.bimg, a.bh, a.bw, 1);
+  PST_CUDA(cudaFuncSetAttribute(conv_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = a.n_mgroups * a.n_ntiles * a.ksplit;
+  conv_wgrad_kernel<<<grid, kThreads, smem, st>>>(tX, tD, a);
+  PST_CUDA(cudaGetLastError());
+}
+
+}  // namespace pst

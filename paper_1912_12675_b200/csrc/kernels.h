@@ -1,0 +1,156 @@
+// kernels.h -- launch interfaces of the hand-written sm_100a kernels of libpst.
+//
+// Layouts:
+//   activations / gradients : NHWC act_t, channels padded to Cp = round_up(C, 16)
+//   conv weight shadows     : fwd   [k*k][Coutp][Cinp] act_t  (K-major B operand)
+//                             dgrad [k*k][Cinp][Coutp] act_t  (taps applied flipped)
+//   master weights          : canonical float32 (OIHW / [out][in]) per stage
+#pragma once
+#include "common.h"
+
+namespace pst {
+
+enum EpiMode { EPI_BN_STATS = 0, EPI_BIAS_ACT = 1, EPI_BIAS_F32 = 2, EPI_DGRAD = 3 };
+
+// One implicit-GEMM convolution on tcgen05 (forward, or dgrad expressed as a
+// stride-1 correlation of dY with the flipped, transposed weights).
+struct ConvSpec {
+  // input tensor (NHWC act_t, channels Cinp), output grid and tensor
+  const act_t* in; int N, H, W, Cinp;
+  int Ho, Wo, Coutp, Cout;
+  int k, S;                 // kernel size, input element stride
+  int off, sgn;             // input coord = out*S + off + sgn*tap  (fwd: -pad,+1; dgrad: +pad,-1)
+  const act_t* wshadow;     // [k*k][Coutp][Cinp]
+  int epi;                  // EpiMode
+  int relu;
+  void* out;                // act_t or float NHWC [N][Ho][Wo][Coutp]
+  const float* bias;        // [Cout] or null
+  double* stats;            // [Coutp][2] (EPI_BN_STATS), accumulated with atomics
+  const act_t* res;         // EPI_DGRAD residual gradient (identity or option A) or null
+  int res_mode;             // 0 none, 1 identity, 2 option A
+  int res_H, res_W, res_C, res_pad;
+};
+void conv_tc(const ConvSpec& c, cudaStream_t st);
+
+// Weight gradient dW[tap*Cinp+ci][co] = sum_pixels X(shifted by tap)[p][ci] * dY[p][co],
+// split over pixel ranges: part[ks][rows][Coutp] float32 (reduced by sgd_update).
+struct WgradSpec {
+  const act_t* x; int N, H, W, Cinp;
+  const act_t* dy; int Ho, Wo, Coutp;
+  int k, S, pad;
+  float* part;              // workspace, ksplit * rows * Coutp floats
+  int ksplit;               // chosen by wgrad_plan
+};
+struct WgradPlan { int ksplit; int64_t part_floats; };
+WgradPlan wgrad_plan(int N, int Ho, int Wo, int Cinp, int Coutp, int k, int num_sm);
+void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st);
+
+// ---------------------------------------------------------------- elementwise / reductions
+// NCHW float32 -> NHWC act_t, channels zero-padded to Cp.
+void input_to_nhwc(const float* x, act_t* out, int N, int C, int H, int W, int Cp, cudaStream_t st);
+
+// BN forward apply (train mode): batch stats from `stats` (sum, sumsq over M values),
+// z = relu?( gamma*(y-mean)*invstd + beta + shortcut(block) ).  Block 0 also writes
+// saved[c] = (mean, invstd) and updates running statistics.
+struct BnApplySpec {
+  const act_t* y; act_t* z; int N, H, W, Cp, C;
+  const double* stats; const float* gamma; const float* beta;
+  float* saved;             // [Cp][2] mean, invstd
+  float* run_mean; float* run_var;
+  float momentum, eps;
+  int relu;
+  // forward shortcut: res [N][res_H][res_W][res_C] (res_C = padded channels, res_Creal real);
+  // identity (mode 1) or option A (mode 2): out channel c reads res channel c - res_pad at (2y, 2x)
+  const act_t* res; int res_mode; int res_H, res_W, res_C, res_Creal, res_pad;
+};
+void bn_apply(const BnApplySpec& s, cudaStream_t st);
+
+// Bias + ReLU forward for convs/FCs without BN is fused in the conv epilogue.
+
+// 2x2/2 max-pool: out [N][H/2][W/2][Cp], arg uint8 (window index 0..3, first max).
+void maxpool2_fwd(const act_t* in, act_t* out, uint8_t* arg, int N, int H, int W, int Cp, cudaStream_t st);
+// Global average pool: [N][H][W][Cp] -> [N][Cp]
+void gap_fwd(const act_t* in, act_t* out, int N, int H, int W, int Cp, cudaStream_t st);
+
+// Backward "pre" kernel for one layer's non-weighted tail, reading the gradient
+// w.r.t. the layer's (pooled) output:
+//   g_z  = pool^T(g_out)           (none / max2 via arg / gap broadcast / H*W)
+//   gpre = g_z * (z > 0)           if relu
+//   if bn: accumulate sums[c] += (sum gpre, sum gpre*xhat), xhat = (y-mean)*invstd
+//   else : accumulate sums[c] += (sum gpre, 0)   (bias gradient)
+// gpre written as act_t [N][H][W][Cp].
+struct BwdPreSpec {
+  const act_t* gout; int pool; const uint8_t* arg;  // pool: 0 none, 1 max2, 2 gap
+  const act_t* z; int relu;
+  const act_t* y; const float* saved; int bn;
+  act_t* gpre; int N, H, W, Cp, C;
+  double* sums;             // [Cp][2]
+  int gout_f32;             // gout is float (loss gradient) instead of act_t
+};
+void bwd_pre(const BwdPreSpec& s, cudaStream_t st);
+
+// BN backward apply: gy = gamma_cur*invstd/M * (M*gpre - S1 - xhat*S2)
+struct BnBwdSpec {
+  const act_t* gpre; const act_t* y; const float* saved; const double* sums;
+  const float* gamma; act_t* gy; int N, H, W, Cp, C;
+};
+void bn_bwd_apply(const BnBwdSpec& s, cudaStream_t st);
+
+// Zero-insertion of a stride-2 gradient: dyd[n][2y][2x][c] = dy[n][y][x][c], else 0.
+void dilate2(const act_t* dy, act_t* dyd, int N, int Ho, int Wo, int H, int W, int Cp, cudaStream_t st);
+
+// Softmax cross-entropy over logits [B][Cp] (first C columns): loss (mean) into
+// loss_ring[(*fwd_counter) % ring], dz = (softmax - onehot)/B as float [B][Cp]
+// (padded columns 0).  Labels come from label_ring[(*fwd_counter) % ring][B].
+// Increments *fwd_counter.
+void softmax_ce(const float* logits, const int32_t* label_ring, int ring, float* loss_ring,
+                int64_t* fwd_counter, float* dz, int B, int C, int Cp, cudaStream_t st);
+
+// ---------------------------------------------------------------- optimiser
+// One SGD-momentum update of a whole stage (PyTorch form): for every canonical
+// parameter, g = (wgrad partial sum | BN/bias double sums | grad buffer),
+// v = mu v + (g + lambda w), w -= lr v, plus the act_t weight shadows.
+// lr = (v_count < n_p ? lr_pipe : lr_np) * gamma^(#milestones <= v_count/spe);
+// the kernel reads and then increments *v_count.
+enum SegKind { SEG_CONVW = 0, SEG_FCW = 1, SEG_VEC = 2 };
+struct SgdSeg {
+  int kind;
+  int64_t off;              // canonical offset in the stage's flat parameter vector
+  int64_t n;                // elements
+  // SEG_CONVW / SEG_FCW
+  int cout, cin, k;         // canonical dims (FC: k = 1)
+  int Coutp, Cinp;          // padded GEMM dims (FC: Cinp = H*W*Cp_in)
+  int fc_C, fc_H, fc_W, fc_Cp;  // FC input tensor geometry for the NCHW-flatten mapping
+  const float* part; int ksplit;  // wgrad partials [ksplit][k*k*Cinp][Coutp]
+  act_t* sh_fwd;            // [k*k][Coutp][Cinp]
+  act_t* sh_bwd;            // [k*k][Cinp][Coutp]
+  // SEG_VEC: gradient = src_d[c*2 + comp] (double sums) for c < n
+  const double* src_d; int comp;
+};
+struct SgdSpec {
+  float* w; float* v;       // stage flat fp32
+  const SgdSeg* segs;       // device array
+  int n_segs;
+  const int64_t* seg_block_start;  // device: first block of each segment (prefix), n_segs+1
+  int64_t total_blocks;
+  int64_t* v_count;         // device version counter of the stage
+  int* ticket;              // device, for last-block increment
+  const float* lr_pipe;     // device scalar: this stage's pipelined lr
+  float lr_np, momentum, wd, gamma;
+  const int64_t* milestones; int n_ms; int64_t spe;
+  const int64_t* n_p;       // device scalar: hybrid switch mini-batch (huge if none)
+};
+void sgd_update(const SgdSpec& s, cudaStream_t st);
+// Writes the shadows from the master weights only (used at create / import).
+void build_shadows(const SgdSpec& s, cudaStream_t st);
+
+}  // namespace pst
+
+namespace pst {
+// ---------------------------------------------------------------- test/debug helpers (ops ABI)
+void nhwc_to_nchw(const void* in, int in_f32, float* out, int N, int C, int H, int W, int Cp, cudaStream_t st);
+void conv_weights_to_shadows(const float* w, int cout, int cin, int k, int Coutp, int Cinp, act_t* sh_fwd,
+                             act_t* sh_bwd, cudaStream_t st);
+void wgrad_reduce(const float* part, int ksplit, int Coutp, int Cinp, int cout, int cin, int k, float* out,
+                  cudaStream_t st);
+}  // namespace pst

@@ -1,0 +1,605 @@
+// pst_api.cu -- the C ABI (include/pst.h): context, step scheduler, hybrid switch,
+// CUDA-graph cache, inter-stage transport (local copies or NCCL send/recv).
+//
+// Schedule (PAPER.md L61/L63/L75, reading AMB-1): at global step t, stage s runs
+// the backward + SGD update of mini-batch b = t-2K+1+s, then the forward of
+// mini-batch f = t-s.  Messages produced at step t are consumed at step t+1:
+// the forward activation of f goes into stage s+1's input ring slot, the input
+// gradient of b into stage s-1's gradient buffer dbuf[b % 2].
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pst.h"
+#include "common.h"
+#include "model.h"
+#include "stage.h"
+
+using namespace pst;
+
+#define PST_NCCL(expr)                                                                       \
+  do {                                                                                       \
+    ncclResult_t r_ = (expr);                                                                \
+    if (r_ != ncclSuccess)                                                                   \
+      throw ::pst::NcclError(std::string(#expr) + ": " + ncclGetErrorString(r_) + " at " +   \
+                             __FILE__ + ":" + std::to_string(__LINE__));                     \
+  } while (0)
+
+namespace {
+
+enum Mode { MODE_PIPE = 0, MODE_NP = 1 };
+
+struct GraphKey {
+  std::vector<int64_t> k;
+  bool operator<(const GraphKey& o) const { return k < o.k; }
+};
+
+}  // namespace
+
+struct pst_ctx {
+  std::string err;
+  int sticky = 0;
+  NetInfo net;
+  std::vector<std::pair<int, int>> ranges;
+  int K = 1;
+  bool dist = false;
+  int rank = 0;
+  ncclComm_t comm = nullptr;
+  std::vector<std::unique_ptr<Stage>> stages;   // local: K stages; dist: 1 (stage == rank)
+  std::vector<int> devices;
+  pst_hparams hp{};
+  std::vector<float> lr_pipe;
+  std::vector<int64_t> milestones;
+  int batch = 0;
+  // schedule state
+  int64_t t = 0, t0 = 0, m0 = 0, n_fed = 0, n_p = INT64_MAX;
+  int mode = MODE_PIPE;
+  bool use_graphs = true;
+  std::vector<std::map<GraphKey, cudaGraphExec_t>> graphs;   // per owned stage
+  std::vector<cudaEvent_t> done;                              // per owned stage: last step's work
+  // host staging (pinned) for the batch
+  float* pin_x[2] = {nullptr, nullptr};
+  int32_t* pin_y[2] = {nullptr, nullptr};
+  cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+  cudaEvent_t pin_ev2[2] = {nullptr, nullptr};
+  int pin_i = 0;
+
+  Stage* stage(int s) {
+    if (!dist) return stages[s].get();
+    return s == rank ? stages[0].get() : nullptr;
+  }
+  int local_index(int s) const { return dist ? 0 : s; }
+  bool owns(int s) const { return !dist || s == rank; }
+};
+
+static thread_local std::string g_last_global_error;
+
+template <typename F>
+static int guard(pst_ctx* ctx, F&& f) {
+  if (ctx && ctx->sticky) return ctx->sticky;
+  try {
+    f();
+    return PST_OK;
+  } catch (const InvalidArg& e) {
+    if (ctx) ctx->err = e.what(); else g_last_global_error = e.what();
+    return PST_E_INVALID;
+  } catch (const Unsupported& e) {
+    if (ctx) ctx->err = e.what(); else g_last_global_error = e.what();
+    return PST_E_UNSUPPORTED;
+  } catch (const StateError& e) {
+    if (ctx) ctx->err = e.what(); else g_last_global_error = e.what();
+    return PST_E_STATE;
+  } catch (const NcclError& e) {
+    if (ctx) { ctx->err = e.what(); ctx->sticky = PST_E_NCCL; } else g_last_global_error = e.what();
+    return PST_E_NCCL;
+  } catch (const CudaError& e) {
+    std::string m = e.what();
+    bool oom = m.find("out of memory") != std::string::npos;
+    if (ctx) { ctx->err = m; if (!oom) ctx->sticky = PST_E_CUDA; } else g_last_global_error = m;
+    return oom ? PST_E_OOM : PST_E_CUDA;
+  } catch (const std::bad_alloc& e) {
+    if (ctx) ctx->err = "host allocation failed"; else g_last_global_error = "host allocation failed";
+    return PST_E_OOM;
+  } catch (const std::exception& e) {
+    if (ctx) { ctx->err = e.what(); ctx->sticky = PST_E_CUDA; } else g_last_global_error = e.what();
+    return PST_E_CUDA;
+  }
+}
+
+// ------------------------------------------------------------------ step programs
+// Enqueue stage s's share of pipelined step t (plan computed by the caller).
+static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& prev_stage,
+                         const StepPlan& next_stage, cudaStream_t st) {
+  Stage* S = c->stage(s);
+  const int K = c->K;
+  if (p.bwd_mb >= 0) {
+    S->enqueue_backward((int)(p.bwd_mb % S->R), (int)(p.bwd_mb & 1), st);
+    if (s > 0 && !c->dist) {
+      Stage* D = c->stage(s - 1);
+      PST_CUDA(cudaMemcpyAsync(D->dbuf((int)(p.bwd_mb & 1)), S->dgrad_out(), D->output_bytes(),
+                               cudaMemcpyDefault, st));
+    }
+  }
+  if (p.fwd_mb >= 0) {
+    S->enqueue_forward((int)(p.fwd_mb % S->R), st);
+    if (s < K - 1 && !c->dist) {
+      Stage* D = c->stage(s + 1);
+      PST_CUDA(cudaMemcpyAsync(D->input_slot((int)(p.fwd_mb % D->R)), S->output_slot((int)(p.fwd_mb % S->R)),
+                               S->output_bytes(), cudaMemcpyDefault, st));
+    }
+  }
+  if (c->dist) {
+    const bool send_f = p.fwd_mb >= 0 && s < K - 1;
+    const bool recv_f = s > 0 && prev_stage.fwd_mb >= 0;
+    const bool send_b = p.bwd_mb >= 0 && s > 0;
+    const bool recv_b = s < K - 1 && next_stage.bwd_mb >= 0;
+    if (send_f || recv_f || send_b || recv_b) {
+      PST_NCCL(ncclGroupStart());
+      if (send_f)
+        PST_NCCL(ncclSend(S->output_slot((int)(p.fwd_mb % S->R)), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+      if (recv_f)
+        PST_NCCL(ncclRecv(S->input_slot((int)(prev_stage.fwd_mb % S->R)), S->input_bytes(), ncclUint8, s - 1,
+                          c->comm, st));
+      if (send_b) PST_NCCL(ncclSend(S->dgrad_out(), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
+      if (recv_b)
+        PST_NCCL(ncclRecv(S->dbuf((int)(next_stage.bwd_mb & 1)), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+      PST_NCCL(ncclGroupEnd());
+    }
+  }
+}
+
+// Non-pipelined (hybrid phase 2) forward or backward part of mini-batch i on stage s.
+static void enqueue_np(pst_ctx* c, int s, int64_t i, bool fwd, cudaStream_t st) {
+  Stage* S = c->stage(s);
+  const int K = c->K;
+  const int slot = (int)(i % S->R);
+  if (fwd) {
+    if (c->dist && s > 0) PST_NCCL(ncclRecv(S->input_slot(slot), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
+    S->enqueue_forward(slot, st);
+    if (s < K - 1) {
+      if (c->dist) {
+        PST_NCCL(ncclSend(S->output_slot(slot), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+      } else {
+        Stage* D = c->stage(s + 1);
+        PST_CUDA(cudaMemcpyAsync(D->input_slot((int)(i % D->R)), S->output_slot(slot), S->output_bytes(),
+                                 cudaMemcpyDefault, st));
+      }
+    }
+  } else {
+    if (c->dist && s < K - 1)
+      PST_NCCL(ncclRecv(S->dbuf((int)(i & 1)), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+    S->enqueue_backward(slot, (int)(i & 1), st);
+    if (s > 0) {
+      if (c->dist) {
+        PST_NCCL(ncclSend(S->dgrad_out(), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
+      } else {
+        Stage* D = c->stage(s - 1);
+        PST_CUDA(cudaMemcpyAsync(D->dbuf((int)(i & 1)), S->dgrad_out(), D->output_bytes(), cudaMemcpyDefault, st));
+      }
+    }
+  }
+}
+
+template <typename F>
+static void run_program(pst_ctx* c, int s, const GraphKey& key, F&& enqueue) {
+  Stage* S = c->stage(s);
+  PST_CUDA(cudaSetDevice(S->dev));
+  if (!c->use_graphs) {
+    enqueue(S->stream);
+    return;
+  }
+  auto& cache = c->graphs[c->local_index(s)];
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    cudaGraph_t g;
+    PST_CUDA(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeRelaxed));
+    try {
+      enqueue(S->stream);
+    } catch (...) {
+      cudaStreamEndCapture(S->stream, &g);
+      throw;
+    }
+    PST_CUDA(cudaStreamEndCapture(S->stream, &g));
+    cudaGraphExec_t ge;
+    PST_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    PST_CUDA(cudaGraphDestroy(g));
+    it = cache.emplace(key, ge).first;
+  }
+  PST_CUDA(cudaGraphLaunch(it->second, S->stream));
+}
+
+// In local mode stage s's step depends on its neighbours' previous step.
+static void wait_neighbours(pst_ctx* c, int s) {
+  if (c->dist) return;
+  Stage* S = c->stage(s);
+  for (int n : {s - 1, s + 1}) {
+    if (n < 0 || n >= c->K) continue;
+    PST_CUDA(cudaStreamWaitEvent(S->stream, c->done[n], 0));
+  }
+}
+
+static void pipe_step(pst_ctx* c) {
+  const int K = c->K;
+  std::vector<StepPlan> plans(K);
+  for (int s = 0; s < K; ++s) plans[s] = plan_step(K, s, c->t, c->t0, c->m0, c->n_fed);
+  // all waits first (events of the previous step), then launches, then records
+  std::vector<int> active;
+  for (int s = 0; s < K; ++s) {
+    if (!c->owns(s)) continue;
+    wait_neighbours(c, s);
+  }
+  for (int s = 0; s < K; ++s) {
+    if (!c->owns(s)) continue;
+    const StepPlan& p = plans[s];
+    const StepPlan prev = s > 0 ? plans[s - 1] : StepPlan{};
+    const StepPlan next = s < K - 1 ? plans[s + 1] : StepPlan{};
+    Stage* S = c->stage(s);
+    GraphKey key;
+    auto slot = [](int64_t mb, int R) { return mb >= 0 ? mb % R : -1; };
+    key.k = {0, slot(p.bwd_mb, S->R), p.bwd_mb >= 0 ? (p.bwd_mb & 1) : -1, slot(p.fwd_mb, S->R),
+             s < K - 1 && p.fwd_mb >= 0 ? p.fwd_mb % ring_slots(K, s + 1) : -1,
+             s > 0 && prev.fwd_mb >= 0 ? slot(prev.fwd_mb, S->R) : -1,
+             s < K - 1 && next.bwd_mb >= 0 ? (next.bwd_mb & 1) : -1};
+    if (p.bwd_mb < 0 && p.fwd_mb < 0 && key.k[5] < 0 && key.k[6] < 0) continue;
+    run_program(c, s, key, [&](cudaStream_t st) { enqueue_pipe(c, s, p, prev, next, st); });
+  }
+  for (int s = 0; s < K; ++s) {
+    if (!c->owns(s)) continue;
+    Stage* S = c->stage(s);
+    PST_CUDA(cudaSetDevice(S->dev));
+    PST_CUDA(cudaEventRecord(c->done[c->local_index(s)], S->stream));
+  }
+  c->t += 1;
+}
+
+static void drain(pst_ctx* c) {
+  if (c->mode != MODE_PIPE) return;
+  // the last backward is stage 0's of mini-batch n_fed-1 at relative step n_fed-1-m0 + 2K-1
+  const int64_t last = c->t0 + (c->n_fed - 1 - c->m0) + 2 * c->K - 1;
+  while (c->n_fed > c->m0 && c->t <= last) pipe_step(c);
+  c->t0 = c->t;
+  c->m0 = c->n_fed;
+}
+
+static void np_step(pst_ctx* c) {
+  const int K = c->K;
+  const int64_t i = c->n_fed - 1;
+  for (int s = 0; s < K; ++s) {
+    if (!c->owns(s)) continue;
+    Stage* S = c->stage(s);
+    if (!c->dist && s > 0) {
+      PST_CUDA(cudaSetDevice(S->dev));
+      PST_CUDA(cudaStreamWaitEvent(S->stream, c->done[s - 1], 0));
+    }
+    GraphKey key;
+    key.k = {1, i % S->R};
+    run_program(c, s, key, [&](cudaStream_t st) { enqueue_np(c, s, i, true, st); });
+    PST_CUDA(cudaEventRecord(c->done[c->local_index(s)], S->stream));
+  }
+  for (int s = K - 1; s >= 0; --s) {
+    if (!c->owns(s)) continue;
+    Stage* S = c->stage(s);
+    if (!c->dist && s < K - 1) {
+      PST_CUDA(cudaSetDevice(S->dev));
+      PST_CUDA(cudaStreamWaitEvent(S->stream, c->done[s + 1], 0));
+    }
+    GraphKey key;
+    key.k = {2, i % S->R, i & 1};
+    run_program(c, s, key, [&](cudaStream_t st) { enqueue_np(c, s, i, false, st); });
+    PST_CUDA(cudaEventRecord(c->done[c->local_index(s)], S->stream));
+  }
+  c->t += 1;
+}
+
+static void sync_all(pst_ctx* c) {
+  for (auto& S : c->stages) {
+    PST_CUDA(cudaSetDevice(S->dev));
+    PST_CUDA(cudaStreamSynchronize(S->stream));
+  }
+}
+
+// ------------------------------------------------------------------ ABI
+extern "C" {
+
+int pst_create(const pst_net* net, const pst_partition* part, const pst_hparams* hp, const pst_dist* dist,
+               pst_ctx** out) {
+  if (!out) return PST_E_INVALID;
+  *out = nullptr;
+  auto* c = new pst_ctx();
+  int rc = guard(nullptr, [&] {
+    PST_CHECK_ARG(net && part && hp, "null argument");
+    PST_CHECK_ARG(net->init_params != nullptr, "init_params is null");
+    c->net = derive_net(*net);
+    PST_CHECK_ARG(net->n_params == c->net.n_params, "n_params does not match the network");
+    c->K = part->n_stages;
+    c->ranges = partition(c->net, c->K, part->ppv);
+    PST_CHECK_ARG(hp->batch >= 1 && hp->batch <= 4096, "batch");
+    PST_CHECK_ARG(hp->lr_pipelined != nullptr, "lr_pipelined");
+    c->batch = hp->batch;
+    c->hp = *hp;
+    c->lr_pipe.assign(hp->lr_pipelined, hp->lr_pipelined + c->K);
+    c->hp.lr_pipelined = c->lr_pipe.data();
+    if (hp->n_milestones > 0) {
+      PST_CHECK_ARG(hp->milestone_epochs != nullptr, "milestones");
+      c->milestones.assign(hp->milestone_epochs, hp->milestone_epochs + hp->n_milestones);
+    }
+    c->hp.milestone_epochs = c->milestones.data();
+    int ndev = 0;
+    PST_CUDA(cudaGetDeviceCount(&ndev));
+    PST_CHECK_ARG(ndev >= 1, "no CUDA device");
+    c->devices.resize(c->K);
+    for (int s = 0; s < c->K; ++s) {
+      c->devices[s] = part->devices ? part->devices[s] : 0;
+      PST_CHECK_ARG(c->devices[s] >= 0 && c->devices[s] < ndev, "device ordinal");
+    }
+    const char* g = std::getenv("PST_GRAPHS");
+    c->use_graphs = !(g && std::string(g) == "0");
+    if (dist) {
+      PST_CHECK_ARG(dist->world == c->K && dist->rank >= 0 && dist->rank < c->K && dist->nccl_id,
+                    "distributed: world must equal n_stages");
+      c->dist = true;
+      c->rank = dist->rank;
+    }
+    for (int s = 0; s < c->K; ++s) {
+      if (!c->owns(s)) continue;
+      c->stages.emplace_back(new Stage(c->net, s, c->K, c->ranges[s].first, c->ranges[s].second, c->devices[s],
+                                       c->hp, net->init_params, c->batch));
+      cudaEvent_t e;
+      PST_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      PST_CUDA(cudaEventRecord(e, c->stages.back()->stream));
+      c->done.push_back(e);
+    }
+    c->graphs.resize(c->stages.size());
+    if (!c->dist) {  // peer access between distinct stage devices (best effort)
+      for (int a = 0; a < c->K; ++a)
+        for (int b = 0; b < c->K; ++b) {
+          if (c->devices[a] == c->devices[b]) continue;
+          int ok = 0;
+          cudaDeviceCanAccessPeer(&ok, c->devices[a], c->devices[b]);
+          if (ok) {
+            cudaSetDevice(c->devices[a]);
+            cudaDeviceEnablePeerAccess(c->devices[b], 0);
+            cudaGetLastError();
+          }
+        }
+    } else {
+      ncclUniqueId id;
+      std::memcpy(&id, dist->nccl_id, sizeof(id));
+      PST_CUDA(cudaSetDevice(c->devices[c->rank]));
+      PST_NCCL(ncclCommInitRank(&c->comm, c->K, id, c->rank));
+    }
+    const size_t xb = (size_t)c->batch * c->net.in_C * c->net.in_H * c->net.in_W;
+    for (int i = 0; i < 2; ++i) {
+      PST_CUDA(cudaMallocHost(&c->pin_x[i], xb * sizeof(float)));
+      PST_CUDA(cudaMallocHost(&c->pin_y[i], c->batch * sizeof(int32_t)));
+      PST_CUDA(cudaEventCreateWithFlags(&c->pin_ev[i], cudaEventDisableTiming));
+      PST_CUDA(cudaEventCreateWithFlags(&c->pin_ev2[i], cudaEventDisableTiming));
+    }
+  });
+  if (rc != PST_OK) {
+    g_last_global_error = c->err.empty() ? g_last_global_error : c->err;
+    pst_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return PST_OK;
+}
+
+int pst_step(pst_ctx* c, const pst_batch* batch) {
+  if (!c) return PST_E_INVALID;
+  return guard(c, [&] {
+    PST_CHECK_ARG(batch != nullptr, "batch is null");
+    if (c->mode == MODE_PIPE && c->n_fed >= c->n_p) {
+      drain(c);
+      c->mode = MODE_NP;
+    }
+    const int64_t mb = c->n_fed;
+    // stage the batch: x into stage 0, labels into the last stage's ring
+    const size_t xb = (size_t)c->batch * c->net.in_C * c->net.in_H * c->net.in_W;
+    const int pi = c->pin_i;
+    c->pin_i ^= 1;
+    Stage* S0 = c->stage(0);
+    Stage* SL = c->stage(c->K - 1);
+    (void)pi;
+    // the pinned slot is reusable once the copies issued two steps ago have executed
+    PST_CUDA(cudaEventSynchronize(c->pin_ev[pi]));
+    PST_CUDA(cudaEventSynchronize(c->pin_ev2[pi]));
+    if (S0) {
+      PST_CHECK_ARG(batch->x != nullptr, "batch x is null");
+      PST_CUDA(cudaSetDevice(S0->dev));
+      if (batch->on_device) {
+        PST_CUDA(cudaMemcpyAsync(S0->stage_x(), batch->x, xb * sizeof(float), cudaMemcpyDeviceToDevice, S0->stream));
+      } else {
+        std::memcpy(c->pin_x[pi], batch->x, xb * sizeof(float));
+        PST_CUDA(cudaMemcpyAsync(S0->stage_x(), c->pin_x[pi], xb * sizeof(float), cudaMemcpyHostToDevice, S0->stream));
+      }
+      PST_CUDA(cudaEventRecord(c->pin_ev[pi], S0->stream));
+    }
+    if (SL) {
+      PST_CHECK_ARG(batch->y != nullptr, "batch y is null");
+      PST_CUDA(cudaSetDevice(SL->dev));
+      if (batch->on_device) {
+        PST_CUDA(cudaMemcpyAsync(SL->label_slot(mb), batch->y, c->batch * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                 SL->stream));
+      } else {
+        std::memcpy(c->pin_y[pi], batch->y, c->batch * sizeof(int32_t));
+        PST_CUDA(cudaMemcpyAsync(SL->label_slot(mb), c->pin_y[pi], c->batch * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, SL->stream));
+      }
+      PST_CUDA(cudaEventRecord(c->pin_ev2[pi], SL->stream));
+    }
+    c->n_fed += 1;
+    if (c->mode == MODE_PIPE) pipe_step(c);
+    else np_step(c);
+  });
+}
+
+int pst_set_hybrid(pst_ctx* c, int64_t switch_epoch) {
+  if (!c) return PST_E_INVALID;
+  return guard(c, [&] {
+    if (c->mode == MODE_NP) throw StateError("already switched to non-pipelined training");
+    const int64_t spe = c->hp.steps_per_epoch > 0 ? c->hp.steps_per_epoch : 1;
+    c->n_p = switch_epoch < 0 ? INT64_MAX : switch_epoch * spe;
+    if (c->n_p < c->n_fed) c->n_p = c->n_fed;  // switch at the next step
+    for (auto& S : c->stages) S->set_n_p(c->n_p);
+  });
+}
+
+int pst_flush(pst_ctx* c) {
+  if (!c) return PST_E_INVALID;
+  return guard(c, [&] { drain(c); });
+}
+
+int pst_weights(pst_ctx* c, uint32_t what, float* out, int64_t cap, int64_t* n) {
+  if (!c || !n) return PST_E_INVALID;
+  return guard(c, [&] {
+    int64_t np = 0, nbn = 0;
+    for (auto& S : c->stages) {
+      np += S->n_params;
+      for (int l = S->l0; l < S->l1; ++l)
+        if (c->net.layers[l].spec.bn) nbn += 2 * c->net.layers[l].spec.cout;
+    }
+    int64_t need = 0;
+    if (what & PST_W_PARAMS) need += np;
+    if (what & PST_W_MOMENTUM) need += np;
+    if (what & PST_W_BNSTATS) need += nbn;
+    *n = need;
+    if (!out) return;
+    PST_CHECK_ARG(cap >= need, "output buffer too small");
+    sync_all(c);
+    int64_t o = 0;
+    if (what & PST_W_PARAMS)
+      for (auto& S : c->stages) { S->read_params(out + o, nullptr); o += S->n_params; }
+    if (what & PST_W_MOMENTUM)
+      for (auto& S : c->stages) { S->read_params(nullptr, out + o); o += S->n_params; }
+    if (what & PST_W_BNSTATS) {
+      std::vector<float> mv;
+      for (auto& S : c->stages) S->read_bnstats(mv);
+      std::memcpy(out + o, mv.data(), mv.size() * sizeof(float));
+    }
+  });
+}
+
+int pst_losses(pst_ctx* c, int64_t first_mb, int64_t n, float* out) {
+  if (!c || (n > 0 && !out) || first_mb < 0 || n < 0) return PST_E_INVALID;
+  return guard(c, [&] {
+    Stage* SL = c->stage(c->K - 1);
+    if (!SL) throw StateError("losses live on the last stage's rank");
+    PST_CHECK_ARG(n <= 1024, "at most 1024 losses are kept");
+    PST_CUDA(cudaSetDevice(SL->dev));
+    PST_CUDA(cudaStreamSynchronize(SL->stream));
+    SL->read_losses(first_mb, n, out);
+  });
+}
+
+int pst_versions(pst_ctx* c, int64_t* v, int32_t cap) {
+  if (!c || !v) return PST_E_INVALID;
+  return guard(c, [&] {
+    PST_CHECK_ARG(cap >= (int32_t)c->stages.size(), "cap");
+    sync_all(c);
+    for (size_t i = 0; i < c->stages.size(); ++i) v[i] = c->stages[i]->read_version();
+  });
+}
+
+int pst_progress(pst_ctx* c, int64_t* steps, int64_t* fed) {
+  if (!c) return PST_E_INVALID;
+  if (steps) *steps = c->t;
+  if (fed) *fed = c->n_fed;
+  return c->sticky ? c->sticky : PST_OK;
+}
+
+int pst_stream(pst_ctx* c, int32_t stage, void** stream) {
+  if (!c || !stream) return PST_E_INVALID;
+  return guard(c, [&] {
+    PST_CHECK_ARG(stage >= 0 && stage < c->K && c->owns(stage), "stage not owned by this context");
+    *stream = (void*)c->stage(stage)->stream;
+  });
+}
+
+int pst_sync(pst_ctx* c) {
+  if (!c) return PST_E_INVALID;
+  return guard(c, [&] { sync_all(c); });
+}
+
+void pst_destroy(pst_ctx* c) {
+  if (!c) return;
+  for (auto& S : c->stages) {
+    cudaSetDevice(S->dev);
+    cudaStreamSynchronize(S->stream);
+  }
+  for (auto& m : c->graphs)
+    for (auto& kv : m) cudaGraphExecDestroy(kv.second);
+  for (auto e : c->done) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (c->pin_x[i]) cudaFreeHost(c->pin_x[i]);
+    if (c->pin_y[i]) cudaFreeHost(c->pin_y[i]);
+    if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
+    if (c->pin_ev2[i]) cudaEventDestroy(c->pin_ev2[i]);
+  }
+  if (c->comm) ncclCommDestroy(c->comm);
+  c->stages.clear();
+  delete c;
+}
+
+const char* pst_last_error(const pst_ctx* c) {
+  if (!c) return g_last_global_error.c_str();
+  return c->err.c_str();
+}
+
+int pst_nccl_unique_id(void* out) {
+  if (!out) return PST_E_INVALID;
+  return guard(nullptr, [&] {
+    static_assert(sizeof(ncclUniqueId) == PST_NCCL_ID_BYTES, "nccl id size");
+    ncclUniqueId id;
+    PST_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int pst_partition_ranges(const pst_net* net, const pst_partition* part, int32_t* ranges) {
+  if (!net || !part || !ranges) return PST_E_INVALID;
+  return guard(nullptr, [&] {
+    NetInfo ni = derive_net(*net);
+    auto r = partition(ni, part->n_stages, part->ppv);
+    for (size_t s = 0; s < r.size(); ++s) {
+      ranges[2 * s] = r[s].first;
+      ranges[2 * s + 1] = r[s].second;
+    }
+  });
+}
+
+int64_t pst_param_count(const pst_net* net) {
+  if (!net) return PST_E_INVALID;
+  int64_t n = -1;
+  int rc = guard(nullptr, [&] { n = derive_net(*net).n_params; });
+  return rc == PST_OK ? n : rc;
+}
+
+int pst_schedule(int32_t K, int32_t s, int64_t t, int64_t n_total, int64_t* bwd_mb, int64_t* fwd_mb,
+                 int64_t* fwd_version) {
+  if (K < 1 || s < 0 || s >= K || t < 0 || !bwd_mb || !fwd_mb || !fwd_version) return PST_E_INVALID;
+  const int64_t nf = n_total < 0 ? INT64_MAX : n_total;
+  StepPlan p = plan_step(K, s, t, 0, 0, std::min<int64_t>(nf, t + 1));
+  *bwd_mb = p.bwd_mb;
+  *fwd_mb = p.fwd_mb;
+  // updates applied by stage s before its forward at step t = backwards at steps <= t
+  // (backward runs first within a step): mini-batches 0 .. t-2K+1+s
+  int64_t done = t - 2 * K + 2 + s;
+  if (done < 0) done = 0;
+  if (done > nf) done = nf;
+  *fwd_version = p.fwd_mb >= 0 ? done : -1;
+  return PST_OK;
+}
+
+const char* pst_build_info(void) {
+  return "libpst sm_100a act=" PST_ACT_NAME " tcgen05+TMA implicit-GEMM conv, NCCL " ;
+}
+
+}  // extern "C"

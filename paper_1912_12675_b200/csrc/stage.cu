@@ -1,0 +1,414 @@
+// stage.cu -- buffers and launch program of one pipeline stage.
+#include "stage.h"
+
+#include <algorithm>
+#include <cstring>
+
+namespace pst {
+
+template <typename T>
+T* Stage::alloc(size_t n, bool zero) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+  if (e != cudaSuccess) throw CudaError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  allocs_.push_back(p);
+  if (zero) PST_CUDA(cudaMemset(p, 0, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, const pst_hparams& hp,
+             const float* init_params, int batch)
+    : s(s_), K(K_), l0(l0_), l1(l1_), dev(device), R(ring_slots(K_, s_)), batch_(batch), net_(net) {
+  PST_CUDA(cudaSetDevice(dev));
+  PST_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  const int B = batch;
+  const int nsm = num_sms(dev);
+  p_base = net.layers[l0].p_begin;
+  n_params = net.layers[l1 - 1].p_end - p_base;
+  w_ = alloc<float>(n_params);
+  v_ = alloc<float>(n_params);
+  PST_CUDA(cudaMemcpy(w_, init_params + p_base, n_params * sizeof(float), cudaMemcpyHostToDevice));
+
+  // input ring of the stage
+  const LayerInfo& f0 = net.layers[l0];
+  for (int r = 0; r < R; ++r) xin_.push_back(alloc<act_t>((size_t)B * f0.in_H * f0.in_W * f0.in_Cp));
+  if (is_first()) xstage_ = alloc<float>((size_t)B * net.in_C * net.in_H * net.in_W);
+
+  // per-layer buffers
+  size_t nrun = 0;
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& li = net.layers[l];
+    if (li.spec.bn) { run_off_.push_back((int64_t)nrun); nrun += 2 * li.Coutp; }
+    fwd_arena_n_ += li.spec.bn ? 2 * li.Coutp : 0;
+    bwd_arena_n_ += 2 * li.Coutp;
+  }
+  run_ = alloc<float>(std::max<size_t>(nrun, 1));
+  {
+    std::vector<float> init(std::max<size_t>(nrun, 1), 0.f);
+    for (int l = l0, b = 0; l < l1; ++l) {
+      const LayerInfo& li = net.layers[l];
+      if (!li.spec.bn) continue;
+      for (int c = 0; c < li.Coutp; ++c) init[run_off_[b] + li.Coutp + c] = 1.f;  // running var = 1
+      ++b;
+    }
+    PST_CUDA(cudaMemcpy(run_, init.data(), init.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  fwd_arena_ = alloc<double>(fwd_arena_n_);
+  bwd_arena_ = alloc<double>(bwd_arena_n_);
+  size_t fo = 0, bo = 0;
+  L_.resize(l1 - l0);
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& li = net.layers[l];
+    LayerBufs& b = L_[l - l0];
+    const size_t out_el = (size_t)B * li.Ho * li.Wo * li.Coutp;
+    const bool last_net = (l == (int)net.layers.size() - 1);
+    for (int r = 0; r < R; ++r) {
+      if (li.spec.bn) b.y.push_back(alloc<act_t>(out_el, false));
+      if (last_net) b.zf.push_back(alloc<float>(out_el));
+      else b.z.push_back(alloc<act_t>(out_el, false));
+      if (li.spec.pool == PST_POOL_MAX2) {
+        b.p.push_back(alloc<act_t>(out_el / 4, false));
+        b.arg.push_back(alloc<uint8_t>(out_el / 4, false));
+      } else if (li.spec.pool == PST_POOL_GAP) {
+        b.p.push_back(alloc<act_t>((size_t)B * li.Coutp, false));
+      }
+      if (li.spec.bn) b.saved.push_back(alloc<float>(2 * li.Coutp));
+    }
+    b.gpre = alloc<act_t>(out_el, false);
+    if (li.spec.bn) b.gy = alloc<act_t>(out_el, false);
+    const bool need_gin = !(is_first() && l == l0);
+    if (need_gin) b.gin = alloc<act_t>((size_t)B * li.in_H * li.in_W * li.in_Cp, false);
+    if (li.spec.kind == PST_LAYER_CONV && li.spec.stride == 2 && need_gin)
+      b.dil = alloc<act_t>((size_t)B * li.in_H * li.in_W * li.Coutp, false);
+    const int kk = li.spec.kind == PST_LAYER_CONV ? li.spec.k : 1;
+    const int wH = li.spec.kind == PST_LAYER_CONV ? li.in_H : 1;
+    WgradPlan wp = wgrad_plan(B, li.Ho, li.Wo, li.Cinp, li.Coutp, kk, nsm);
+    (void)wH;
+    b.ksplit = wp.ksplit;
+    b.wpart = alloc<float>((size_t)wp.part_floats, false);
+    // weight shadows (+ the 3xTF32 lo plane right after the raw plane in the split build)
+    b.sh_fwd = alloc<act_t>((size_t)kk * kk * li.Coutp * li.Cinp * (PST_SPLIT ? 2 : 1));
+    b.sh_bwd = alloc<act_t>((size_t)kk * kk * li.Coutp * li.Cinp * (PST_SPLIT ? 2 : 1));
+    if (li.spec.bn) { b.stats = fwd_arena_ + fo; fo += 2 * li.Coutp; }
+    b.sums = bwd_arena_ + bo; bo += 2 * li.Coutp;
+  }
+  const LayerInfo& lastl = net.layers[l1 - 1];
+  if (!is_last()) {
+    const size_t ob = (size_t)B * lastl.out_H * lastl.out_W * ((lastl.out_C + 15) / 16 * 16);
+    dbuf_[0] = alloc<act_t>(ob);
+    dbuf_[1] = alloc<act_t>(ob);
+  } else {
+    label_ring_n_ = 2 * K + 2;
+    label_ring_ = alloc<int32_t>((size_t)label_ring_n_ * B);
+    loss_ring_ = alloc<float>(1024);
+    fwd_counter_ = alloc<int64_t>(1);
+    dz_ = alloc<float>((size_t)B * lastl.Coutp);
+  }
+
+  // ---- optimiser segments
+  std::vector<SgdSeg> segs;
+  std::vector<int64_t> starts;
+  int64_t blocks = 0;
+  auto add = [&](SgdSeg g) {
+    starts.push_back(blocks);
+    blocks += (g.n + 255) / 256;
+    segs.push_back(g);
+  };
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& li = net.layers[l];
+    LayerBufs& b = L_[l - l0];
+    SgdSeg g{};
+    g.off = li.off_W - p_base;
+    g.n = li.n_W;
+    g.cout = li.spec.cout;
+    g.cin = li.spec.cin;
+    g.Coutp = li.Coutp;
+    g.Cinp = li.Cinp;
+    g.part = b.wpart;
+    g.ksplit = b.ksplit;
+    g.sh_fwd = b.sh_fwd;
+    g.sh_bwd = b.sh_bwd;
+    if (li.spec.kind == PST_LAYER_CONV) {
+      g.kind = SEG_CONVW;
+      g.k = li.spec.k;
+    } else {
+      g.kind = SEG_FCW;
+      g.k = 1;
+      g.fc_C = li.in_C; g.fc_H = li.in_H; g.fc_W = li.in_W; g.fc_Cp = li.in_Cp;
+    }
+    add(g);
+    if (li.spec.bias) {
+      SgdSeg v{}; v.kind = SEG_VEC; v.off = li.off_b - p_base; v.n = li.spec.cout; v.src_d = b.sums; v.comp = 0;
+      add(v);
+    }
+    if (li.spec.bn) {
+      SgdSeg gg{}; gg.kind = SEG_VEC; gg.off = li.off_g - p_base; gg.n = li.spec.cout; gg.src_d = b.sums; gg.comp = 1;
+      add(gg);
+      SgdSeg bb{}; bb.kind = SEG_VEC; bb.off = li.off_be - p_base; bb.n = li.spec.cout; bb.src_d = b.sums; bb.comp = 0;
+      add(bb);
+    }
+  }
+  starts.push_back(blocks);
+  d_segs_ = alloc<SgdSeg>(segs.size());
+  PST_CUDA(cudaMemcpy(d_segs_, segs.data(), segs.size() * sizeof(SgdSeg), cudaMemcpyHostToDevice));
+  d_seg_start_ = alloc<int64_t>(starts.size());
+  PST_CUDA(cudaMemcpy(d_seg_start_, starts.data(), starts.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  d_vcount_ = alloc<int64_t>(1);
+  d_ticket_ = alloc<int>(1);
+  d_lr_ = alloc<float>(1);
+  PST_CUDA(cudaMemcpy(d_lr_, &hp.lr_pipelined[s], sizeof(float), cudaMemcpyHostToDevice));
+  d_np_ = alloc<int64_t>(1);
+  set_n_p(INT64_MAX);
+  d_ms_ = alloc<int64_t>(std::max(1, hp.n_milestones));
+  if (hp.n_milestones > 0)
+    PST_CUDA(cudaMemcpy(d_ms_, hp.milestone_epochs, hp.n_milestones * sizeof(int64_t), cudaMemcpyHostToDevice));
+  sgd_.w = w_;
+  sgd_.v = v_;
+  sgd_.segs = d_segs_;
+  sgd_.n_segs = (int)segs.size();
+  sgd_.seg_block_start = d_seg_start_;
+  sgd_.total_blocks = blocks;
+  sgd_.v_count = d_vcount_;
+  sgd_.ticket = d_ticket_;
+  sgd_.lr_pipe = d_lr_;
+  sgd_.lr_np = hp.lr_nonpipelined;
+  sgd_.momentum = hp.momentum;
+  sgd_.wd = hp.weight_decay;
+  sgd_.gamma = hp.gamma;
+  sgd_.milestones = d_ms_;
+  sgd_.n_ms = hp.n_milestones;
+  sgd_.spe = hp.steps_per_epoch > 0 ? hp.steps_per_epoch : INT64_MAX;
+  sgd_.n_p = d_np_;
+  build_shadows(sgd_, stream);
+  PST_CUDA(cudaStreamSynchronize(stream));
+}
+
+Stage::~Stage() {
+  cudaSetDevice(dev);
+  if (stream) cudaStreamSynchronize(stream);
+  for (void* p : allocs_) cudaFree(p);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void Stage::set_n_p(int64_t n_p) {
+  PST_CUDA(cudaSetDevice(dev));
+  PST_CUDA(cudaMemcpy(d_np_, &n_p, sizeof(int64_t), cudaMemcpyHostToDevice));
+}
+
+act_t* Stage::in_tensor(int l, int slot) const {
+  return l == l0 ? xin_[slot] : out_tensor(l - 1, slot);
+}
+act_t* Stage::out_tensor(int l, int slot) const {
+  const LayerBufs& b = L_[l - l0];
+  if (!b.p.empty()) return b.p[slot];
+  return b.z.empty() ? nullptr : b.z[slot];
+}
+act_t* Stage::output_slot(int slot) const { return out_tensor(l1 - 1, slot); }
+act_t* Stage::dgrad_out() const { return L_[0].gin; }
+size_t Stage::input_bytes() const {
+  const LayerInfo& f0 = net_.layers[l0];
+  return (size_t)batch_ * f0.in_H * f0.in_W * f0.in_Cp * sizeof(act_t);
+}
+size_t Stage::output_bytes() const {
+  const LayerInfo& li = net_.layers[l1 - 1];
+  return (size_t)batch_ * li.out_H * li.out_W * ((li.out_C + 15) / 16 * 16) * sizeof(act_t);
+}
+size_t Stage::stage_x_bytes() const {
+  return (size_t)batch_ * net_.in_C * net_.in_H * net_.in_W * sizeof(float);
+}
+
+// ------------------------------------------------------------------ forward
+void Stage::enqueue_forward(int slot, cudaStream_t st) {
+  const int B = batch_;
+  if (fwd_arena_n_) PST_CUDA(cudaMemsetAsync(fwd_arena_, 0, fwd_arena_n_ * sizeof(double), st));
+  if (is_first())
+    input_to_nhwc(xstage_, xin_[slot], B, net_.in_C, net_.in_H, net_.in_W, net_.in_Cp, st);
+  int bn_local = 0;
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& li = net_.layers[l];
+    LayerBufs& b = L_[l - l0];
+    const bool last_net = (l == (int)net_.layers.size() - 1);
+    const bool conv = li.spec.kind == PST_LAYER_CONV;
+    ConvSpec c{};
+    c.in = in_tensor(l, slot);
+    c.N = B;
+    c.H = conv ? li.in_H : 1;
+    c.W = conv ? li.in_W : 1;
+    c.Cinp = li.Cinp;
+    c.Ho = li.Ho; c.Wo = li.Wo; c.Coutp = li.Coutp; c.Cout = li.spec.cout;
+    c.k = conv ? li.spec.k : 1;
+    c.S = conv ? li.spec.stride : 1;
+    c.off = conv ? -li.spec.pad : 0;
+    c.sgn = 1;
+    c.wshadow = b.sh_fwd;
+    c.relu = li.spec.relu;
+    c.bias = li.spec.bias ? w_ + (li.off_b - p_base) : nullptr;
+    if (li.spec.bn) {
+      c.epi = EPI_BN_STATS;
+      c.out = b.y[slot];
+      c.stats = b.stats;
+      c.relu = 0;
+    } else if (last_net) {
+      c.epi = EPI_BIAS_F32;
+      c.out = b.zf[slot];
+    } else {
+      c.epi = EPI_BIAS_ACT;
+      c.out = b.z[slot];
+    }
+    conv_tc(c, st);
+    if (li.spec.bn) {
+      BnApplySpec a{};
+      a.y = b.y[slot]; a.z = b.z[slot];
+      a.N = B; a.H = li.Ho; a.W = li.Wo; a.Cp = li.Coutp; a.C = li.spec.cout;
+      a.stats = b.stats;
+      a.gamma = w_ + (li.off_g - p_base);
+      a.beta = w_ + (li.off_be - p_base);
+      a.saved = b.saved[slot];
+      a.run_mean = run_ + run_off_[bn_local];
+      a.run_var = run_ + run_off_[bn_local] + li.Coutp;
+      a.momentum = 0.1f; a.eps = 1e-5f;
+      a.relu = li.spec.relu;
+      if (li.spec.residual) {
+        const LayerInfo& src = net_.layers[li.block_src];
+        a.res = in_tensor(li.block_src, slot);
+        a.res_mode = li.res_mode;
+        a.res_H = src.in_H; a.res_W = src.in_W; a.res_C = src.in_Cp; a.res_Creal = src.in_C;
+        a.res_pad = li.res_pad;
+      }
+      bn_apply(a, st);
+      ++bn_local;
+    }
+    if (li.spec.pool == PST_POOL_MAX2)
+      maxpool2_fwd(b.z[slot], b.p[slot], b.arg[slot], B, li.Ho, li.Wo, li.Coutp, st);
+    else if (li.spec.pool == PST_POOL_GAP)
+      gap_fwd(b.z[slot], b.p[slot], B, li.Ho, li.Wo, li.Coutp, st);
+    if (last_net)
+      softmax_ce(b.zf[slot], label_ring_, label_ring_n_, loss_ring_, fwd_counter_, dz_, B,
+                 li.spec.cout, li.Coutp, st);
+  }
+}
+
+// ------------------------------------------------------------------ backward + update
+void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
+  const int B = batch_;
+  PST_CUDA(cudaMemsetAsync(bwd_arena_, 0, bwd_arena_n_ * sizeof(double), st));
+  for (int l = l1 - 1; l >= l0; --l) {
+    const LayerInfo& li = net_.layers[l];
+    LayerBufs& b = L_[l - l0];
+    const bool last_net = (l == (int)net_.layers.size() - 1);
+    const bool conv = li.spec.kind == PST_LAYER_CONV;
+    BwdPreSpec pr{};
+    if (last_net) {
+      pr.gout = reinterpret_cast<const act_t*>(dz_);
+      pr.gout_f32 = 1;
+    } else if (l == l1 - 1) {
+      pr.gout = dbuf_[dpar];
+    } else {
+      pr.gout = L_[l + 1 - l0].gin;
+    }
+    pr.pool = li.spec.pool;
+    pr.arg = li.spec.pool == PST_POOL_MAX2 ? b.arg[slot] : nullptr;
+    pr.z = b.z.empty() ? nullptr : b.z[slot];
+    pr.relu = li.spec.relu;
+    pr.bn = li.spec.bn;
+    pr.y = li.spec.bn ? b.y[slot] : nullptr;
+    pr.saved = li.spec.bn ? b.saved[slot] : nullptr;
+    pr.gpre = b.gpre;
+    pr.N = B; pr.H = li.Ho; pr.W = li.Wo; pr.Cp = li.Coutp; pr.C = li.spec.cout;
+    pr.sums = b.sums;
+    bwd_pre(pr, st);
+    const act_t* dY = b.gpre;
+    if (li.spec.bn) {
+      BnBwdSpec bb{};
+      bb.gpre = b.gpre; bb.y = b.y[slot]; bb.saved = b.saved[slot]; bb.sums = b.sums;
+      bb.gamma = w_ + (li.off_g - p_base);  // current gamma (no stash)
+      bb.gy = b.gy;
+      bb.N = B; bb.H = li.Ho; bb.W = li.Wo; bb.Cp = li.Coutp; bb.C = li.spec.cout;
+      bn_bwd_apply(bb, st);
+      dY = b.gy;
+    }
+    // weight gradient from the saved input of this mini-batch
+    WgradSpec wg{};
+    wg.x = in_tensor(l, slot);
+    wg.N = B;
+    wg.H = conv ? li.in_H : 1;
+    wg.W = conv ? li.in_W : 1;
+    wg.Cinp = li.Cinp;
+    wg.dy = dY; wg.Ho = li.Ho; wg.Wo = li.Wo; wg.Coutp = li.Coutp;
+    wg.k = conv ? li.spec.k : 1;
+    wg.S = conv ? li.spec.stride : 1;
+    wg.pad = conv ? li.spec.pad : 0;
+    wg.part = b.wpart;
+    wg.ksplit = b.ksplit;
+    conv_wgrad_tc(wg, st);
+    // input gradient with the CURRENT weights
+    if (b.gin != nullptr) {
+      ConvSpec c{};
+      const act_t* src = dY;
+      int sH = li.Ho, sW = li.Wo;
+      if (conv && li.spec.stride == 2) {
+        dilate2(dY, b.dil, B, li.Ho, li.Wo, li.in_H, li.in_W, li.Coutp, st);
+        src = b.dil; sH = li.in_H; sW = li.in_W;
+      }
+      c.in = src; c.N = B;
+      c.H = conv ? sH : 1; c.W = conv ? sW : 1;
+      c.Cinp = li.Coutp;
+      c.Ho = conv ? li.in_H : 1; c.Wo = conv ? li.in_W : 1;
+      c.Coutp = li.Cinp;
+      c.Cout = conv ? li.in_C : li.Cinp;
+      c.k = conv ? li.spec.k : 1;
+      c.S = 1;
+      c.off = conv ? li.spec.pad : 0;
+      c.sgn = -1;
+      c.wshadow = b.sh_bwd;
+      c.epi = EPI_DGRAD;
+      c.out = b.gin;
+      if (li.spec.block_begin && li.block_end >= 0) {
+        const LayerInfo& e = net_.layers[li.block_end];
+        c.res = L_[li.block_end - l0].gpre;
+        c.res_mode = e.res_mode;
+        c.res_H = e.Ho; c.res_W = e.Wo; c.res_C = e.Coutp; c.res_pad = e.res_pad;
+      }
+      conv_tc(c, st);
+    }
+  }
+  sgd_update(sgd_, st);
+}
+
+// ------------------------------------------------------------------ host readback
+void Stage::read_params(float* out_params, float* out_mom) const {
+  PST_CUDA(cudaSetDevice(dev));
+  if (out_params) PST_CUDA(cudaMemcpy(out_params, w_, n_params * sizeof(float), cudaMemcpyDeviceToHost));
+  if (out_mom) PST_CUDA(cudaMemcpy(out_mom, v_, n_params * sizeof(float), cudaMemcpyDeviceToHost));
+}
+
+void Stage::read_bnstats(std::vector<float>& mv) const {
+  PST_CUDA(cudaSetDevice(dev));
+  int b = 0;
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& li = net_.layers[l];
+    if (!li.spec.bn) continue;
+    std::vector<float> tmp(2 * li.Coutp);
+    PST_CUDA(cudaMemcpy(tmp.data(), run_ + run_off_[b], tmp.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    mv.insert(mv.end(), tmp.begin(), tmp.begin() + li.spec.cout);
+    mv.insert(mv.end(), tmp.begin() + li.Coutp, tmp.begin() + li.Coutp + li.spec.cout);
+    ++b;
+  }
+}
+
+int64_t Stage::read_version() const {
+  PST_CUDA(cudaSetDevice(dev));
+  int64_t v = 0;
+  PST_CUDA(cudaMemcpy(&v, d_vcount_, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return v;
+}
+
+void Stage::read_losses(int64_t first_mb, int64_t n, float* out) const {
+  PST_CUDA(cudaSetDevice(dev));
+  std::vector<float> ring(1024);
+  PST_CUDA(cudaMemcpy(ring.data(), loss_ring_, 1024 * sizeof(float), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n; ++i) out[i] = ring[(first_mb + i) % 1024];
+}
+
+}  // namespace pst

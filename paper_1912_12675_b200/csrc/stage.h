@@ -1,0 +1,101 @@
+// stage.h -- one pipeline stage: the contiguous weighted layers p_{s}+1..p_{s+1}
+// with their weights (one copy, no stash: P:L35/L236), momentum,
+// the saved-activation ring (activations kept until the stage's backward),
+// and the launch program for its forward and backward(+update) passes.
+#pragma once
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+#include "model.h"
+
+namespace pst {
+
+struct LayerBufs {
+  std::vector<act_t*> y, z, p;   // per ring slot: conv out (BN input), post-op, pooled
+  std::vector<float*> zf;        // per slot: float logits (last FC)
+  std::vector<uint8_t*> arg;     // per slot: max-pool argmax
+  std::vector<float*> saved;     // per slot: BN (mean, invstd) [Coutp][2]
+  act_t* gpre = nullptr;         // gradient w.r.t. pre-activation (after pool^T, relu^T)
+  act_t* gy = nullptr;           // gradient w.r.t. conv output (after BN^T)
+  act_t* gin = nullptr;          // gradient w.r.t. the layer input
+  act_t* dil = nullptr;          // zero-inserted gradient for stride-2 dgrad
+  float* wpart = nullptr;        // wgrad split-K partials
+  int ksplit = 1;
+  double* stats = nullptr;       // forward BN sums [Coutp][2]
+  double* sums = nullptr;        // backward sums [Coutp][2]
+  act_t* sh_fwd = nullptr;       // [k*k][Coutp][Cinp]
+  act_t* sh_bwd = nullptr;       // [k*k][Cinp][Coutp]
+};
+
+class Stage {
+ public:
+  Stage(const NetInfo& net, int s, int K, int l0, int l1, int device, const pst_hparams& hp,
+        const float* init_params, int batch);
+  ~Stage();
+  Stage(const Stage&) = delete;
+  Stage& operator=(const Stage&) = delete;
+
+  // Enqueue work (capturable): forward of the mini-batch whose saved state lives in `slot`.
+  void enqueue_forward(int slot, cudaStream_t st);
+  // Backward + SGD update of the mini-batch in `slot`, reading the output gradient
+  // from dbuf[dpar] (non-last stages) or the stored dz (last stage).
+  void enqueue_backward(int slot, int dpar, cudaStream_t st);
+
+  act_t* input_slot(int slot) const { return xin_[slot]; }
+  act_t* output_slot(int slot) const;            // stage output tensor (non-last stages)
+  act_t* dgrad_out() const;                      // gradient w.r.t. the stage input
+  act_t* dbuf(int par) const { return dbuf_[par]; }
+  size_t input_bytes() const;
+  size_t output_bytes() const;
+  float* stage_x() const { return xstage_; }     // stage 0: float NCHW staging of the batch
+  size_t stage_x_bytes() const;
+  int32_t* label_slot(int64_t mb) const { return label_ring_ + (mb % label_ring_n_) * batch_; }
+
+  void set_n_p(int64_t n_p);
+  // Synchronous host copies (call only when the stream is idle).
+  void read_params(float* out_params, float* out_mom) const;   // canonical stage block
+  void read_bnstats(std::vector<float>& mean_var) const;       // per BN layer: mean[C], var[C]
+  int64_t read_version() const;
+  void read_losses(int64_t first_mb, int64_t n, float* out) const;
+
+  const int s, K, l0, l1, dev, R, batch_;
+  int64_t p_base = 0, n_params = 0;
+  cudaStream_t stream = nullptr;
+  bool is_first() const { return s == 0; }
+  bool is_last() const { return l1 == (int)net_.layers.size(); }
+
+ private:
+  const NetInfo& net_;
+  std::vector<void*> allocs_;
+  template <typename T> T* alloc(size_t n, bool zero = true);
+  act_t* in_tensor(int l, int slot) const;
+  act_t* out_tensor(int l, int slot) const;
+
+  std::vector<LayerBufs> L_;
+  std::vector<act_t*> xin_;
+  act_t* dbuf_[2] = {nullptr, nullptr};
+  float* xstage_ = nullptr;
+  float* w_ = nullptr;
+  float* v_ = nullptr;
+  float* run_ = nullptr;          // per local BN layer: mean[Coutp], var[Coutp]
+  std::vector<int64_t> run_off_;
+  double* fwd_arena_ = nullptr; size_t fwd_arena_n_ = 0;
+  double* bwd_arena_ = nullptr; size_t bwd_arena_n_ = 0;
+  // last stage
+  int32_t* label_ring_ = nullptr; int label_ring_n_ = 0;
+  float* loss_ring_ = nullptr;
+  int64_t* fwd_counter_ = nullptr;
+  float* dz_ = nullptr;
+  // optimiser
+  SgdSpec sgd_{};
+  SgdSeg* d_segs_ = nullptr;
+  int64_t* d_seg_start_ = nullptr;
+  int64_t* d_vcount_ = nullptr;
+  int* d_ticket_ = nullptr;
+  float* d_lr_ = nullptr;
+  int64_t* d_np_ = nullptr;
+  int64_t* d_ms_ = nullptr;
+};
+
+}  // namespace pst

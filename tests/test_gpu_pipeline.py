@@ -1,0 +1,97 @@
+"""Pipeline parity (GPU): libpst.so's stale-weight pipelined training against the
+oracle's schedule (Oracle B), step by step, on identical seeded inputs.
+
+Every K-stage configuration here runs all stages on cuda:0 ("local" mode: the
+same scheduler and stage programs as the multi-GPU path; transfers are device
+copies instead of NCCL).  Checked after EVERY pipeline step: each parameter
+tensor within 2e-3 relative (inf-norm) and every mini-batch loss within 1e-2
+(BASELINE.json north_star tolerances, reading AMB-21), plus the stage version
+counters against the closed form.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import pst_workloads as W
+from tests.parity import (L_TOL, W_TOL, flat_params, hparams, loss_errors, oracle_run, tensor_errors)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pst():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1912_12675_b200 as p
+    return p
+
+
+def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, spe=1 << 62,
+             milestones=(), per_step=True, seed=5):
+    K = len(ppv) + 1
+    flat = W.init_params(net, seed=seed)
+    data = W.batches(net.in_shape, B, N, seed=seed + 100)
+    lr_np = lr[-1] if lr_np is None else lr_np
+    hp = hparams(lr, K, lr_np, mom, wd, milestones, 0.1, spe)
+    ref = oracle_run(net, flat, ppv, data, hp, n_p=n_p, snapshot=per_step)
+    pipe = pst.Pipeline(net, flat, ppv, B, lr, lr_np, momentum=mom, weight_decay=wd, milestones=milestones,
+                        steps_per_epoch=spe)
+    if n_p is not None:
+        assert n_p % spe == 0
+        pipe.set_hybrid(n_p // spe)
+    worst = (0.0, None)
+    t = 0
+    for i, (x, y) in enumerate(data):
+        pipe.step(x, y)
+        if per_step:
+            # a hybrid switch inserts the drain steps before this mini-batch's step
+            steps, _ = pipe.progress()
+            while t < steps - 1:
+                t += 1
+            e = tensor_errors(net, pipe.weights(), flat_params(net, ref.snapshots[steps - 1]))
+            worst = max(worst, e, key=lambda z: z[0])
+            t = steps
+    pipe.flush()
+    e = tensor_errors(net, pipe.weights(), flat_params(net, ref.params))
+    worst = max(worst, e, key=lambda z: z[0])
+    lerr = loss_errors(pipe.losses(0, N), ref.losses)
+    vers = pipe.versions()
+    pipe.close()
+    return worst, lerr, vers, ref
+
+
+@pytest.mark.parametrize("K,ppv", [(1, ()), (2, (3,)), (3, (1, 3))])
+def test_tiny_resnet_pipeline(pst, K, ppv):
+    net = W.tiny_resnet(width=16, hw=8, n=1)
+    worst, lerr, vers, _ = run_both(pst, net, ppv, 32, 8, [0.05] * (K - 1) + [0.1])
+    assert worst[0] <= W_TOL, worst
+    assert lerr <= L_TOL, lerr
+    assert list(vers) == [8] * K
+
+
+@pytest.mark.parametrize("K,ppv", [(1, ()), (2, (2,)), (4, (1, 2, 3))])
+def test_tiny_cnn_pipeline(pst, K, ppv):
+    net = W.tiny_cnn(hw=8)
+    worst, lerr, vers, _ = run_both(pst, net, ppv, 32, 8, [0.05] * K, wd=5e-4)
+    assert worst[0] <= W_TOL, worst
+    assert lerr <= L_TOL, lerr
+
+
+def test_lenet5_config1_k2(pst):
+    """BASELINE.json configs[0]: LeNet-5, MNIST-shaped, batch 64, 2 stages, 20 steps."""
+    cfg = W.CONFIGS["lenet5"]
+    worst, lerr, vers, _ = run_both(pst, W.lenet5(), cfg.ppv[2], 64, 20, cfg.lr_vector(2), mom=cfg.momentum,
+                                    wd=cfg.weight_decay)
+    assert worst[0] <= W_TOL, worst
+    assert lerr <= L_TOL, lerr
+
+
+def test_hybrid_switch(pst):
+    """pipelined for n_p mini-batches, drain, then non-pipelined (AMB-10)."""
+    net = W.tiny_resnet(width=16, hw=8, n=1)
+    worst, lerr, vers, ref = run_both(pst, net, (1, 3), 32, 9, [0.02, 0.05, 0.1], lr_np=0.08, n_p=4, spe=2,
+                                      milestones=(3,))
+    assert worst[0] <= W_TOL, worst
+    assert lerr <= L_TOL, lerr
+    assert list(vers) == [9, 9, 9]
