@@ -1,0 +1,318 @@
+#!/usr/bin/env python3
+"""Benchmark: pipelined stale-weight training throughput on B200 (BASELINE.json metric).
+
+    python bench.py --gpus N --steps K --warmup W            (N>1: under torch.distributed.run)
+    python bench.py --impl reference --gpus N --steps K --warmup W
+
+Workload: ResNet-110, CIFAR-10-shaped synthetic data, batch 128 (BASELINE.json
+configs[3], the paper's headline ResNet-110 case), split into
+K = N pipeline stages, one per GPU (PPV from pst_workloads.CONFIGS; N=1 is
+non-pipelined training on one GPU).  One step = one global pipeline step: every
+stage runs the backward+update of one mini-batch and the forward of another, so
+the job trains `batch` images per step; value = steps * batch / device time
+(max over ranks).  Prints ONE JSON line on rank 0.
+
+The reference arm for this tier is the CPU oracle (oracle/, the only other place
+bench.py executes it): each step trains a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+
+METRIC = "train images/sec at 1/2/4/8 B200 stages; speedup vs 1-GPU; conv tensor-pipe %"
+PAPER_IMG_S = {1: 760.0, 2: 1321.0}   # ResNet-110 on GTX1060, context only
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="resnet110")
+    p.add_argument("--batch", type=int, default=0)
+    p.add_argument("--profile-steps", type=int, default=2)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=16, help="images per oracle sample step")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        if self.p is None:
+            return out
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 5]
+        os.unlink(self.f.name)
+        if not rows:
+            return out
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].strip().lower() == "active"})
+        out.update(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=max(mx) if mx else None,
+                   reasons=reasons, samples=len(rows))
+        return out
+
+
+# --------------------------------------------------------------------------- CPU oracle (baseline)
+def oracle_sample_rate(cfg, sample_b, n_steps=1, seed=42):
+    """Train `n_steps` non-pipelined oracle steps on a sample_b-image slice; img/s."""
+    import pst_workloads as W
+    from oracle import network as Net, pipeline as Pl, layers as Lx
+    net = cfg.netspec()
+    flat = W.init_params(net, seed=seed)
+    st = Net.CNNStage(net.layers, first_stage=True)
+    params = Net.unflatten(net.layers, flat)
+    hp = Pl.HParams(lr_pipelined=[cfg.base_lr], lr_nonpipelined=cfg.base_lr, momentum=cfg.momentum,
+                    weight_decay=cfg.weight_decay)
+    data = [W.make_batch(net.in_shape, sample_b, i, seed=1234) for i in range(n_steps)]
+    t0 = time.perf_counter()
+    Pl.run_sgd(st, params, data, hp)
+    dt = time.perf_counter() - t0
+    return n_steps * sample_b / dt, dt
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        return int(max(n)) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, rank, world):
+    import pst_workloads as W
+    if rank != 0:
+        return
+    cfg = W.CONFIGS[args.config]
+    B = args.batch or cfg.batch
+    sample = args.cpu_sample
+    for _ in range(args.warmup):
+        oracle_sample_rate(cfg, sample, 1)
+    tot = 0.0
+    for _ in range(args.steps):
+        _, dt = oracle_sample_rate(cfg, sample, 1)
+        tot += dt
+    rate = args.steps * sample / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "img/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps * (B / sample),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.net}_cifar10_b{B}", "model": cfg.net, "global_batch": B,
+                   "stages": 1, "parallelism": "none (CPU oracle)"},
+        "cpu_baseline": {"value": rate, "unit": "img/s", "cores": blas_threads(), "kind": "oracle",
+                         "sample": f"1 non-pipelined SGD step of {cfg.net} on a {sample}-image slice per step"},
+        "e2e": {"value": rate, "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import pst_workloads as W
+    import paper_1912_12675_b200 as pst
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    cfg = W.CONFIGS[args.config]
+    K = world
+    if K not in cfg.ppv:
+        raise SystemExit(f"no PPV for {K} stages in config {cfg.name}")
+    ppv = cfg.ppv[K]
+    B = args.batch or cfg.batch
+    net = cfg.netspec()
+    params = W.init_params(net, seed=42)
+    lr = cfg.lr_vector(K)
+    kw = dict(momentum=cfg.momentum, weight_decay=cfg.weight_decay, milestones=cfg.milestones,
+              steps_per_epoch=cfg.steps_per_epoch)
+    if world > 1:
+        nid = [pst.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        pipe = pst.Pipeline(net, params, ppv, B, lr, cfg.base_lr, devices=list(range(K)), rank=rank,
+                            nccl_id=nid[0], **kw)
+        my_stage = rank
+    else:
+        pipe = pst.Pipeline(net, params, ppv, B, lr, cfg.base_lr, **kw)
+        my_stage = 0
+    stream = torch.cuda.ExternalStream(pipe.stream(my_stage))
+
+    n_pool = 8
+    host = [W.make_batch(net.in_shape, B, i, seed=1234) for i in range(n_pool)]
+    dev = [(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()) for x, y in host]
+    torch.cuda.synchronize()
+
+    warm = max(args.warmup, 2 * K)   # reach the pipeline's steady state before timing
+    for i in range(warm):
+        pipe.step(*dev[i % n_pool])
+    pipe.sync()
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- device-timed region: inputs resident in HBM
+    clocks = ClockSampler(local)
+    l0 = pipe.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0.record(stream)
+    for i in range(args.steps):
+        pipe.step(*dev[(warm + i) % n_pool])
+    e1.record(stream)
+    pipe.sync()
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = pipe.launches() - l0
+    clk = clocks.stop()
+    value = args.steps * B / (ms / 1e3)
+
+    # ---- instrumented window: CUDA events around every kernel (eager launches)
+    pipe.profile(True)
+    for i in range(args.profile_steps):
+        pipe.step(*dev[i % n_pool])
+    prof = pipe.profile_read()
+    pipe.profile(False)
+    pk = peaks()
+    cls = max(prof, key=lambda k: prof[k][0])
+    kms, kn, kbytes, kflops = prof[cls]
+    achieved = kbytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(cls)
+        except Exception:
+            traffic = None
+    step_ms_prof = sum(v[0] for v in prof.values()) / max(1, args.profile_steps)
+    roofline = {"bound": "hbm", "kernel": cls, "achieved": achieved, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+                "frac": achieved / pk.get("hbm_gbs", 6555.8), "traffic": traffic,
+                "alg_bytes_per_launch": kbytes / max(1, kn), "launches": kn, "avg_launch_us": 1e3 * kms / max(1, kn),
+                "share_of_step": (kms / max(1, args.profile_steps)) / step_ms_prof if step_ms_prof else None,
+                "tensor_tflops": kflops / (kms / 1e3) / 1e12 if kms > 0 else 0.0,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+    kernel_table = {k: {"ms_per_step": v[0] / max(1, args.profile_steps), "launches_per_step": v[1] / max(1, args.profile_steps),
+                        "GBps": (v[2] / (v[0] / 1e3) / 1e9) if v[0] > 0 else 0.0,
+                        "TFLOPs": (v[3] / (v[0] / 1e3) / 1e12) if v[0] > 0 else 0.0}
+                    for k, v in prof.items() if v[1] > 0}
+
+    # ---- end-to-end through the public API: host buffers, H2D + loss readback every step
+    e2e = None
+    if not args.no_e2e:
+        last = (rank == K - 1) if world > 1 else True
+        torch.cuda.synchronize()
+        barrier()
+        steps0, fed0 = pipe.progress()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            x, y = host[i % n_pool]
+            pipe.step(x, y)
+            if last:
+                mb = fed0 + i - (K - 1)
+                if mb >= 0:
+                    pipe.losses(mb, 1)
+        pipe.sync()
+        dt = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": args.steps * B / dt, "unit": "img/s",
+               "h2d_bytes_per_step": int(host[0][0].nbytes + host[0][1].nbytes), "d2h_bytes_per_step": 4}
+
+    # ---- CPU oracle baseline (rank 0, N == 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, dt = oracle_sample_rate(cfg, args.cpu_sample, 1)
+        cpu = {"value": rate, "unit": "img/s", "cores": blas_threads(), "kind": "oracle",
+               "sample": f"1 non-pipelined SGD step of {cfg.net} on a {args.cpu_sample}-image slice "
+                         f"({dt:.1f} s, float64 NumPy)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "img/s", "n_gpus": world, "steps": args.steps,
+            "warmup": warm, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": (value / PAPER_IMG_S[world]) if world in PAPER_IMG_S else None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.net}_cifar10_b{B}_pp{K}", "model": cfg.net, "global_batch": B,
+                       "stages": K, "ppv": list(ppv), "parallelism": f"pp{K}" if K > 1 else "none",
+                       "precision": "fp32 storage, 3xTF32 tensor-core products (" + pst.build_info() + ")",
+                       "l2": "inputs larger than L2 (saved-activation ring >> 126 MB)",
+                       "lr_per_stage": lr},
+            "clocks": clk, "gpu_launches": launches, "roofline": roofline, "kernels": kernel_table,
+            "e2e": e2e, "cpu_baseline": cpu,
+            "paper_context": {"img_s_1gpu_gtx1060": 760, "img_s_2gpu_gtx1060": 1321, "source": "PAPER.md L192"},
+        }
+        print(json.dumps(line), flush=True)
+    pipe.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

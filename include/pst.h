@@ -177,6 +177,23 @@ int pst_stream(pst_ctx* ctx, int32_t stage, void** stream);
 /* Blocks until all queued work of this context has finished. */
 int pst_sync(pst_ctx* ctx);
 
+/* Kernels launched by the library so far in this process (graph replays counted
+ * by the kernels captured in each graph). */
+int pst_launches(pst_ctx* ctx, int64_t* n);
+
+/* Kernel classes for pst_profile_read. */
+typedef enum { PST_K_CONV_FWD = 0, PST_K_CONV_DGRAD, PST_K_CONV_WGRAD, PST_K_BN_APPLY, PST_K_BWD_PRE,
+               PST_K_BN_BWD, PST_K_POOL, PST_K_SGD, PST_K_LOSS, PST_K_MISC, PST_K_NCLASSES } pst_kernel_class;
+
+/* enable != 0: later steps run eagerly (no CUDA graphs) with a CUDA-event pair
+ * around every kernel launch; counters are reset.  enable == 0: back to graphs. */
+int pst_profile(pst_ctx* ctx, int32_t enable);
+/* Totals since pst_profile(ctx, 1) for one kernel class: event-timed milliseconds,
+ * launches, and the algorithmic bytes / FLOPs of those launches (DESIGN.md
+ * "Roofline accounting").  Synchronises. */
+int pst_profile_read(pst_ctx* ctx, int32_t cls, double* ms, int64_t* launches, double* bytes,
+                     double* flops);
+
 void pst_destroy(pst_ctx* ctx);
 const char* pst_last_error(const pst_ctx* ctx);
 

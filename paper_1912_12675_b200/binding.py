@@ -87,6 +87,10 @@ def lib():
         "pst_schedule": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, P(C.c_int64),
                                    P(C.c_int64), P(C.c_int64)]),
         "pst_build_info": (C.c_char_p, []),
+        "pst_launches": (C.c_int, [C.c_void_p, P(C.c_int64)]),
+        "pst_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+        "pst_profile_read": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_double), P(C.c_int64), P(C.c_double),
+                                       P(C.c_double)]),
         "pst_op_conv2d_fwd": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 8),
         "pst_op_conv2d_dgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 8),
         "pst_op_conv2d_wgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 8),
@@ -260,6 +264,26 @@ class Pipeline:
 
     def sync(self):
         self._c(lib().pst_sync(self._ctx))
+
+    def launches(self) -> int:
+        n = C.c_int64()
+        self._c(lib().pst_launches(self._ctx, C.byref(n)))
+        return n.value
+
+    def profile(self, enable: bool):
+        self._c(lib().pst_profile(self._ctx, 1 if enable else 0))
+
+    KERNEL_CLASSES = ("conv_fwd", "conv_dgrad", "conv_wgrad", "bn_apply", "bwd_pre", "bn_bwd", "pool", "sgd",
+                      "loss", "misc")
+
+    def profile_read(self):
+        """{class: (ms, launches, alg_bytes, alg_flops)} since profile(True)."""
+        out = {}
+        for i, name in enumerate(self.KERNEL_CLASSES):
+            ms, n, b, f = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+            self._c(lib().pst_profile_read(self._ctx, i, C.byref(ms), C.byref(n), C.byref(b), C.byref(f)))
+            out[name] = (ms.value, n.value, b.value, f.value)
+        return out
 
     def close(self):
         if getattr(self, "_ctx", None):

@@ -3,6 +3,7 @@
 
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <vector>
 
 namespace pst {
 
@@ -47,9 +48,62 @@ CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void* gaddr, const
 }
 
 int num_sms(int device) {
+  static int cache[64] = {0};
+  if (device >= 0 && device < 64 && cache[device]) return cache[device];
   int n = 0;
   PST_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+  if (device >= 0 && device < 64) cache[device] = n;
   return n;
 }
+
+namespace prof {
+thread_local int64_t launches = 0;
+bool enabled = false;
+namespace {
+struct Rec { cudaEvent_t a, b; int cls; double bytes, flops; };
+std::vector<Rec> pending;
+cudaEvent_t open_ev = nullptr;
+double tot_ms[NCLS], tot_bytes[NCLS], tot_flops[NCLS];
+int64_t tot_n[NCLS];
+}  // namespace
+
+void begin(cudaStream_t st) {
+  ++launches;
+  if (!enabled) return;
+  PST_CUDA(cudaEventCreate(&open_ev));
+  PST_CUDA(cudaEventRecord(open_ev, st));
+}
+
+void end(cudaStream_t st, int cls, double b, double f) {
+  if (!enabled || !open_ev) return;
+  cudaEvent_t e;
+  PST_CUDA(cudaEventCreate(&e));
+  PST_CUDA(cudaEventRecord(e, st));
+  pending.push_back({open_ev, e, cls, b, f});
+  open_ev = nullptr;
+}
+
+void read(int cls, double* ms, int64_t* n, double* bytes, double* flops) {
+  for (Rec& r : pending) {
+    float t = 0.f;
+    PST_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    tot_ms[r.cls] += t;
+    tot_bytes[r.cls] += r.bytes;
+    tot_flops[r.cls] += r.flops;
+    tot_n[r.cls] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  pending.clear();
+  if (cls < 0 || cls >= NCLS) {
+    for (int i = 0; i < NCLS; ++i) tot_ms[i] = tot_bytes[i] = tot_flops[i] = 0, tot_n[i] = 0;
+    return;
+  }
+  if (ms) *ms = tot_ms[cls];
+  if (n) *n = tot_n[cls];
+  if (bytes) *bytes = tot_bytes[cls];
+  if (flops) *flops = tot_flops[cls];
+}
+}  // namespace prof
 
 }  // namespace pst

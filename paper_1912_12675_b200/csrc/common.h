@@ -118,4 +118,15 @@ CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void* gaddr, const
 
 int num_sms(int device);
 
+// Launch accounting and optional per-kernel CUDA-event timing (bench.py's roofline).
+namespace prof {
+enum Cls { CONV_FWD = 0, CONV_DGRAD, CONV_WGRAD, BN_APPLY, BWD_PRE, BN_BWD, POOL, SGD, LOSS, MISC, NCLS };
+extern thread_local int64_t launches;  // kernels enqueued by this thread (graph capture included)
+extern bool enabled;                   // when true, launchers bracket kernels with events
+void begin(cudaStream_t st);
+void end(cudaStream_t st, int cls, double alg_bytes, double alg_flops);
+// Resolves pending events (caller synchronised).  cls < 0 resets everything.
+void read(int cls, double* ms, int64_t* n, double* bytes, double* flops);
+}  // namespace prof
+
 }  // namespace pst

@@ -634,8 +634,16 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
   int dev;
   PST_CUDA(cudaGetDevice(&dev));
   const int grid = std::min(a.n_tiles, num_sms(dev));
+  const double es = sizeof(act_t);
+  const double bytes = (double)c.N * c.H * c.W * c.Cinp * es +
+                       (double)c.N * c.Ho * c.Wo * c.Coutp * (c.epi == EPI_BIAS_F32 ? 4.0 : es) +
+                       (double)a.taps * c.Coutp * c.Cinp * es * (PST_SPLIT ? 2 : 1) +
+                       (c.res ? (double)c.N * c.res_H * c.res_W * c.res_C * es : 0.0);
+  const double flops = 2.0 * c.N * c.Ho * c.Wo * c.Coutp * (double)c.Cinp * a.taps;
+  prof::begin(st);
   conv_fwd_kernel<<<grid, kThreads, smem, st>>>(tA, tB, tBlo, a);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, c.epi == EPI_DGRAD ? prof::CONV_DGRAD : prof::CONV_FWD, bytes, flops);
 }
 
 WgradPlan wgrad_plan(int N, int Ho, int Wo, int Cinp, int Coutp, int k, int num_sm) {
@@ -686,8 +694,14 @@ void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
   CUtensorMap tD = act_tmap(w.dy, w.N, w.Ho, w.Wo, w.Coutp, a.bimg, a.bh, a.bw, 1);
   PST_CUDA(cudaFuncSetAttribute(conv_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = a.n_mgroups * a.n_ntiles * a.ksplit;
+  const double es = sizeof(act_t);
+  const double bytes = (double)w.N * w.H * w.W * w.Cinp * es + (double)w.N * w.Ho * w.Wo * w.Coutp * es +
+                       (double)a.ksplit * a.rows * w.Coutp * 4.0;
+  const double flops = 2.0 * a.rows * (double)w.Coutp * w.N * w.Ho * w.Wo;
+  prof::begin(st);
   conv_wgrad_kernel<<<grid, kThreads, smem, st>>>(tX, tD, a);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::CONV_WGRAD, bytes, flops);
 }
 
 }  // namespace pst

@@ -455,26 +455,34 @@ __global__ void sgd_kernel(const SgdSpec s) {
 }  // namespace
 
 void input_to_nhwc(const float* x, act_t* out, int N, int C, int H, int W, int Cp, cudaStream_t st) {
+  prof::begin(st);
   input_to_nhwc_kernel<<<grid_for((int64_t)N * H * W), kBlock, 0, st>>>(x, out, N, C, H, W, Cp);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::MISC, (double)N * H * W * (C * 4.0 + Cp * sizeof(act_t)), 0);
 }
 
 void bn_apply(const BnApplySpec& s, cudaStream_t st) {
   const int64_t nvec = (int64_t)s.N * s.H * s.W * (s.Cp / 8);
+  prof::begin(st);
   bn_apply_kernel<<<grid_for(nvec), kBlock, 2 * s.Cp * sizeof(float), st>>>(s);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::BN_APPLY, (double)nvec * 8 * sizeof(act_t) * (s.res_mode ? 3 : 2), 0);
 }
 
 void maxpool2_fwd(const act_t* in, act_t* out, uint8_t* arg, int N, int H, int W, int Cp, cudaStream_t st) {
   PST_CHECK_ARG(H % 2 == 0 && W % 2 == 0, "maxpool2 needs even H, W");
   const int64_t nvec = (int64_t)N * (H / 2) * (W / 2) * (Cp / 8);
+  prof::begin(st);
   maxpool2_kernel<<<grid_for(nvec), kBlock, 0, st>>>(in, out, arg, N, H, W, Cp);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::POOL, (double)nvec * 8 * (5 * sizeof(act_t) + 1), 0);
 }
 
 void gap_fwd(const act_t* in, act_t* out, int N, int H, int W, int Cp, cudaStream_t st) {
+  prof::begin(st);
   gap_kernel<<<grid_for((int64_t)N * Cp), kBlock, 0, st>>>(in, out, N, H, W, Cp);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::POOL, (double)N * Cp * (H * W + 1) * sizeof(act_t), 0);
 }
 
 void bwd_pre(const BwdPreSpec& s, cudaStream_t st) {
@@ -485,31 +493,41 @@ void bwd_pre(const BwdPreSpec& s, cudaStream_t st) {
   if (block == 0) block = kBlock;
   const int64_t nvec = (int64_t)s.N * s.H * s.W * cv;
   const int g = grid_for(nvec, block);
+  prof::begin(st);
   bwd_pre_kernel<<<g, block, 2 * s.Cp * sizeof(float), st>>>(s);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::BWD_PRE, (double)nvec * 8 * sizeof(act_t) * (2 + (s.relu ? 1 : 0) + (s.bn ? 1 : 0)), 0);
 }
 
 void bn_bwd_apply(const BnBwdSpec& s, cudaStream_t st) {
   const int64_t nvec = (int64_t)s.N * s.H * s.W * (s.Cp / 8);
+  prof::begin(st);
   bn_bwd_apply_kernel<<<grid_for(nvec), kBlock, 5 * s.Cp * sizeof(float), st>>>(s);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::BN_BWD, (double)nvec * 8 * sizeof(act_t) * 3, 0);
 }
 
 void dilate2(const act_t* dy, act_t* dyd, int N, int Ho, int Wo, int H, int W, int Cp, cudaStream_t st) {
   const int64_t nvec = (int64_t)N * H * W * (Cp / 8);
+  prof::begin(st);
   dilate2_kernel<<<grid_for(nvec), kBlock, 0, st>>>(dy, dyd, N, Ho, Wo, H, W, Cp);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::MISC, (double)nvec * 8 * sizeof(act_t) * 1.25, 0);
 }
 
 void softmax_ce(const float* logits, const int32_t* label_ring, int ring, float* loss_ring,
                 int64_t* fwd_counter, float* dz, int B, int C, int Cp, cudaStream_t st) {
+  prof::begin(st);
   softmax_ce_kernel<<<1, 512, 0, st>>>(logits, label_ring, ring, loss_ring, fwd_counter, dz, B, C, Cp);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::LOSS, (double)B * Cp * 8.0, 0);
 }
 
 void sgd_update(const SgdSpec& s, cudaStream_t st) {
+  prof::begin(st);
   sgd_kernel<true><<<(unsigned)s.total_blocks, kBlock, 0, st>>>(s);
   PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::SGD, (double)s.total_blocks * kBlock * 4.0 * 5, 0);
 }
 
 void build_shadows(const SgdSpec& s, cudaStream_t st) {

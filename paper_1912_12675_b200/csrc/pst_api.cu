@@ -40,6 +40,10 @@ struct GraphKey {
   std::vector<int64_t> k;
   bool operator<(const GraphKey& o) const { return k < o.k; }
 };
+struct GraphEntry {
+  cudaGraphExec_t exec;
+  int64_t kernels;  // kernel launches captured in the graph
+};
 
 }  // namespace
 
@@ -62,7 +66,7 @@ struct pst_ctx {
   int64_t t = 0, t0 = 0, m0 = 0, n_fed = 0, n_p = INT64_MAX;
   int mode = MODE_PIPE;
   bool use_graphs = true;
-  std::vector<std::map<GraphKey, cudaGraphExec_t>> graphs;   // per owned stage
+  std::vector<std::map<GraphKey, GraphEntry>> graphs;        // per owned stage
   std::vector<cudaEvent_t> done;                              // per owned stage: last step's work
   // host staging (pinned) for the batch
   float* pin_x[2] = {nullptr, nullptr};
@@ -191,7 +195,7 @@ template <typename F>
 static void run_program(pst_ctx* c, int s, const GraphKey& key, F&& enqueue) {
   Stage* S = c->stage(s);
   PST_CUDA(cudaSetDevice(S->dev));
-  if (!c->use_graphs) {
+  if (!c->use_graphs || prof::enabled) {   // profiling runs eagerly: events bracket each kernel
     enqueue(S->stream);
     return;
   }
@@ -199,6 +203,7 @@ static void run_program(pst_ctx* c, int s, const GraphKey& key, F&& enqueue) {
   auto it = cache.find(key);
   if (it == cache.end()) {
     cudaGraph_t g;
+    const int64_t before = prof::launches;
     PST_CUDA(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeRelaxed));
     try {
       enqueue(S->stream);
@@ -207,12 +212,15 @@ static void run_program(pst_ctx* c, int s, const GraphKey& key, F&& enqueue) {
       throw;
     }
     PST_CUDA(cudaStreamEndCapture(S->stream, &g));
+    const int64_t nk = prof::launches - before;
+    prof::launches = before;  // counted per replay below
     cudaGraphExec_t ge;
     PST_CUDA(cudaGraphInstantiate(&ge, g, 0));
     PST_CUDA(cudaGraphDestroy(g));
-    it = cache.emplace(key, ge).first;
+    it = cache.emplace(key, GraphEntry{ge, nk}).first;
   }
-  PST_CUDA(cudaGraphLaunch(it->second, S->stream));
+  PST_CUDA(cudaGraphLaunch(it->second.exec, S->stream));
+  prof::launches += it->second.kernels;
 }
 
 // In local mode stage s's step depends on its neighbours' previous step.
@@ -535,7 +543,7 @@ void pst_destroy(pst_ctx* c) {
     cudaStreamSynchronize(S->stream);
   }
   for (auto& m : c->graphs)
-    for (auto& kv : m) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : m) cudaGraphExecDestroy(kv.second.exec);
   for (auto e : c->done) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
     if (c->pin_x[i]) cudaFreeHost(c->pin_x[i]);
@@ -596,6 +604,30 @@ int pst_schedule(int32_t K, int32_t s, int64_t t, int64_t n_total, int64_t* bwd_
   if (done > nf) done = nf;
   *fwd_version = p.fwd_mb >= 0 ? done : -1;
   return PST_OK;
+}
+
+int pst_launches(pst_ctx* c, int64_t* n) {
+  if (!c || !n) return PST_E_INVALID;
+  *n = prof::launches;
+  return PST_OK;
+}
+
+int pst_profile(pst_ctx* c, int32_t enable) {
+  if (!c) return PST_E_INVALID;
+  return guard(c, [&] {
+    sync_all(c);
+    prof::read(-1, nullptr, nullptr, nullptr, nullptr);
+    prof::enabled = enable != 0;
+  });
+}
+
+int pst_profile_read(pst_ctx* c, int32_t cls, double* ms, int64_t* launches, double* bytes, double* flops) {
+  if (!c) return PST_E_INVALID;
+  return guard(c, [&] {
+    PST_CHECK_ARG(cls >= 0 && cls < prof::NCLS, "kernel class");
+    sync_all(c);
+    prof::read(cls, ms, launches, bytes, flops);
+  });
 }
 
 const char* pst_build_info(void) {
