@@ -53,6 +53,7 @@ struct FwdArgs {
   double* stats;
   const act_t* res;
   int res_mode, res_H, res_W, res_C, res_pad;
+  int a4, b3;   // tensor-map forms (act_tmap / w_tmap)
 };
 
 __device__ __forceinline__ void decode_tile_px(const FwdArgs& a, int mt, int row, int& n, int& y,
@@ -78,19 +79,45 @@ __device__ __forceinline__ void split_lo(const uint8_t* raw, uint8_t* lo, uint32
   }
 }
 
-__device__ __forceinline__ void store16(void* dst, const float* v) {
-#if PST_SPLIT
-  float4* op = reinterpret_cast<float4*>(dst);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-#else
+// 16 consecutive channels c0..c0+15 of one pixel into a channel-planar tensor:
+// plane (c/EPC) at stride npix*16 bytes.
+__device__ __forceinline__ void store16_planar(act_t* base, int64_t npix, int64_t pix, int c0, const float* v) {
   alignas(16) act_t h[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) h[i] = f2act(v[i]);
-  uint4* op = reinterpret_cast<uint4*>(dst);
 #pragma unroll
-  for (int i = 0; i < (int)(16 * sizeof(act_t) / 16); ++i) op[i] = reinterpret_cast<uint4*>(h)[i];
-#endif
+  for (int j = 0; j < 16 / kEPC; ++j)
+    *reinterpret_cast<uint4*>(base + ((int64_t)(c0 / kEPC + j) * npix + pix) * kEPC) =
+        reinterpret_cast<const uint4*>(h)[j];
+}
+__device__ __forceinline__ void store16_f32(float* base, int64_t npix, int64_t pix, int c0, const float* v) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *reinterpret_cast<float4*>(base + ((int64_t)(c0 / 4 + j) * npix + pix) * 4) =
+        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+__device__ __forceinline__ float ld_planar(const act_t* base, int64_t npix, int64_t pix, int c) {
+  return act2f(base[((int64_t)(c / kEPC) * npix + pix) * kEPC + c % kEPC]);
+}
+
+// load one activation box (act_tmap): x/y in pixels (may be negative: zero fill), image n0, plane cc
+__device__ __forceinline__ void tma_act(void* dst, const CUtensorMap* tm, uint64_t* bar, bool is4d, int x, int y,
+                                        int n0, int cc) {
+  if (is4d) ptx::tma_load_4d(dst, tm, bar, x * kEPC, y, n0, cc);
+  else ptx::tma_load_5d(dst, tm, bar, 0, x, y, n0, cc);
+}
+// load one weight box (w_tmap): rows co0.., planes cc.., tap
+__device__ __forceinline__ void tma_w(void* dst, const CUtensorMap* tm, uint64_t* bar, bool is3d, int co0, int cc,
+                                      int tap) {
+  if (is3d) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(ptx::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(ptx::smem_u32(bar)), "r"(co0 * kEPC), "r"(cc), "r"(tap)
+        : "memory");
+  } else {
+    ptx::tma_load_4d(dst, tm, bar, 0, co0, cc, tap);
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -153,15 +180,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_expect_tx(&full[st], a.tx_bytes);
             uint8_t* sa = ring + st * a.stage_bytes;
             uint8_t* sb = sa + a.a_bytes;
-            for (int j = 0; j < nch; ++j) {
-              const int cc = kcc * nch + j;
-              ptx::tma_load_5d(sa + j * 2048, &tmA, &full[st], 0, cc, x0 + a.sgn * s, y0 + a.sgn * r, n0);
-              ptx::tma_load_4d(sb + j * (a.BN * 16), &tmB, &full[st], 0, cc, nt * a.BN, tap);
+            const int cc = kcc * nch;
+            // one box each: A = nch planes x 128 pixels (rows of contiguous pixels), B = nch x BN rows
+            tma_act(sa, &tmA, &full[st], a.a4, x0 + a.sgn * s, y0 + a.sgn * r, n0, cc);
+            tma_w(sb, &tmB, &full[st], a.b3, nt * a.BN, cc, tap);
 #if PST_SPLIT
-              ptx::tma_load_4d(sb + a.a_bytes + a.b_bytes + j * (a.BN * 16), &tmBlo, &full[st], 0, cc,
-                               nt * a.BN, tap);
+            tma_w(sb + a.a_bytes + a.b_bytes, &tmBlo, &full[st], a.b3, nt * a.BN, cc, tap);
 #endif
-            }
             if (++st == a.stages) { st = 0; ph ^= 1; }
           }
         }
@@ -223,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       decode_tile_px(a, mt, row, n, y, x);
       const bool valid = (n < a.N) && (y < a.Ho) && (x < a.Wo);
       const int64_t pix = ((int64_t)n * a.Ho + y) * a.Wo + x;
+      const int64_t npix = (int64_t)a.N * a.Ho * a.Wo;
       for (int ch = 0; ch < a.BN / 16; ++ch) {
         float v[16];
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * a.BN + ch * 16;
@@ -246,26 +272,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {  // EPI_DGRAD: + shortcut^T of the residual layer's gradient
           if (valid && a.res_mode == 1) {
-            const act_t* rp = a.res + pix * a.Coutp + c0;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += act2f(rp[i]);
+            for (int i = 0; i < 16; ++i) v[i] += ld_planar(a.res, npix, pix, c0 + i);
           } else if (valid && a.res_mode == 2 && ((y | x) & 1) == 0) {
             const int64_t rpix = ((int64_t)n * a.res_H + (y >> 1)) * a.res_W + (x >> 1);
+            const int64_t rnpix = (int64_t)a.N * a.res_H * a.res_W;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const int c = c0 + i;
-              if (c < a.Cout) v[i] += act2f(a.res[rpix * a.res_C + c + a.res_pad]);
+              if (c < a.Cout) v[i] += ld_planar(a.res, rnpix, rpix, c + a.res_pad);
             }
           }
         }
         if (valid) {
-          if (a.epi == EPI_BIAS_F32) {
-            float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + pix * a.Coutp + c0);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-          } else {
-            store16(reinterpret_cast<act_t*>(a.out) + pix * a.Coutp + c0, v);
-          }
+          if (a.epi == EPI_BIAS_F32) store16_f32(reinterpret_cast<float*>(a.out), npix, pix, c0, v);
+          else store16_planar(reinterpret_cast<act_t*>(a.out), npix, pix, c0, v);
         }
         if (a.epi == EPI_BN_STATS) {
           // per-channel sums over the 128 pixel rows via an smem transpose
@@ -376,6 +397,7 @@ struct WgArgs {
   uint32_t x_bytes, d_bytes, stage_bytes;
   uint32_t tmem_cols;
   float* part;
+  int x4, d4;   // act_tmap forms
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -436,13 +458,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_expect_tx(&full[st], used_x + used_d);
         uint8_t* sx = ring + st * a.stage_bytes;
         uint8_t* sd = sx + a.x_bytes;
-        for (int j = 0; j < bn_c; ++j)
-          ptx::tma_load_5d(sd + j * (kWgPix * 16), &tmD, &full[st], 0, nt * bn_c + j, xo, yo, n0);
+        tma_act(sd, &tmD, &full[st], a.d4, xo, yo, n0, nt * bn_c);   // all bn_c planes, one box
         for (int qq = q0; qq < q1; ++qq) {
           const int tap = qq / cin_c, cc = qq % cin_c;
           const int r = tap / a.k, s = tap % a.k;
-          ptx::tma_load_5d(sx + (qq - q0) * (kWgPix * 16), &tmX, &full[st], 0, cc, xo * a.S - a.pad + s,
-                           yo * a.S - a.pad + r, n0);
+          tma_act(sx + (qq - q0) * (kWgPix * 16), &tmX, &full[st], a.x4, xo * a.S - a.pad + s,
+                  yo * a.S - a.pad + r, n0, cc);
         }
         if (++st == a.stages) { st = 0; ph ^= 1; }
       }
@@ -539,6 +560,209 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- weight gradient, 3xTF32 build
+// One K stage = P output pixels (nb images x bh rows x Wo cols).  Two TMA boxes per
+// stage: the dY tile (all bn_c planes) and the input band that every tap of those
+// pixels reads (band_r x band_c pixels per image, the group's channel planes).  The
+// converter warpgroup then builds, in shared memory, the K-major hi/lo operand rows
+// (tap, ci) x P -- the 9-fold tap replication happens in smem, not through TMA.
+struct WbArgs {
+  int N, H, W, Cinp, Ho, Wo, Coutp;
+  int k, S, pad;
+  int nb, bh, P, P8, band_r, band_c, ny, n_units;
+  int rows, n_mt, G, n_mgroups, BNw, n_ntiles, ksplit;
+  int pl_grp, pl_all;   // X planes per box; whether every group loads all planes
+  int stages;
+  uint32_t rawx_bytes, rawx_tx, rawd_bytes, a_bytes, d_bytes, stage_bytes, sbo;
+  uint32_t tmem_cols;
+  float* part;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_wgrad_band_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD,
+                           const WbArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // stage: [raw X][raw dY][A hi][A lo][D hi][D lo]
+  uint8_t* ring = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.stages * a.stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kMaxStages;
+  uint64_t* ready = bars + 2 * kMaxStages;
+  uint64_t* tfull = bars + 3 * kMaxStages;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int b = blockIdx.x;
+  const int mg = b % a.n_mgroups;
+  const int nt = (b / a.n_mgroups) % a.n_ntiles;
+  const int ks = b / (a.n_mgroups * a.n_ntiles);
+  const int u_lo = (int)((int64_t)ks * a.n_units / a.ksplit);
+  const int u_hi = (int)((int64_t)(ks + 1) * a.n_units / a.ksplit);
+  const int mt0 = mg * a.G;
+  const int g_cnt = min(a.G, a.n_mt - mt0);
+  const int r0 = mt0 * 128;
+  const int r_end = min(r0 + g_cnt * 128, a.rows);
+  const int pl0 = a.pl_all ? 0 : (r0 % a.Cinp) / kEPC;
+  const int bn_c = a.BNw / kEPC;
+  const int n_iter = u_hi - u_lo;
+  const uint32_t off_rawd = a.rawx_bytes;
+  const uint32_t off_a = off_rawd + a.rawd_bytes;
+  const uint32_t off_d = off_a + 2 * a.a_bytes;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.stages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+      ptx::mbar_init(&ready[i], 4);
+    }
+    ptx::mbar_init(&tfull[0], 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_ptr, a.tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr;
+
+  if (warp == 0) {
+    if (lane == 0 && n_iter > 0) {
+      ptx::prefetch_tmap(&tmX);
+      ptx::prefetch_tmap(&tmD);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = u_lo; u < u_hi; ++u) {
+        const int n0 = (u / a.ny) * a.nb, y0 = (u % a.ny) * a.bh;
+        ptx::mbar_wait(&empty[st], ph ^ 1);
+        ptx::mbar_expect_tx(&full[st], a.rawx_tx + a.rawd_bytes);
+        uint8_t* s0 = ring + st * a.stage_bytes;
+        ptx::tma_load_4d(s0, &tmX, &full[st], -a.pad * kEPC, y0 * a.S - a.pad, n0, pl0);
+        ptx::tma_load_4d(s0 + off_rawd, &tmD, &full[st], 0, y0, n0, nt * bn_c);
+        if (++st == a.stages) { st = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_iter > 0) {
+      const uint32_t idesc = ptx::idesc_mma(128, a.BNw, 0, 0, PST_AB_FORMAT);
+      const uint32_t mtile = 16 * a.sbo;   // 128 rows
+      int st = 0;
+      uint32_t ph = 0;
+      for (int it = 0; it < n_iter; ++it) {
+        ptx::mbar_wait(&ready[st], ph);
+        ptx::tc_fence_after();
+        const uint32_t s0 = ptx::smem_u32(ring + st * a.stage_bytes);
+        const uint32_t ahi = s0 + off_a, alo = ahi + a.a_bytes, dhi = s0 + off_d, dlo = dhi + a.d_bytes;
+        for (int j = 0; j < g_cnt; ++j) {
+          const uint32_t dt = tmem_base + j * a.BNw;
+          for (int kk = 0; kk < a.P8 / 8; ++kk) {
+            const uint64_t ad = ptx::smem_desc(ahi + j * mtile + kk * 256, 128, a.sbo);
+            const uint64_t adl = ptx::smem_desc(alo + j * mtile + kk * 256, 128, a.sbo);
+            const uint64_t bd = ptx::smem_desc(dhi + kk * 256, 128, a.sbo);
+            const uint64_t bdl = ptx::smem_desc(dlo + kk * 256, 128, a.sbo);
+            ptx::umma(dt, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+            ptx::umma(dt, ad, bdl, idesc, 1u);
+            ptx::umma(dt, adl, bd, idesc, 1u);
+          }
+        }
+        ptx::umma_commit(&empty[st]);
+        if (++st == a.stages) { st = 0; ph ^= 1; }
+      }
+      ptx::umma_commit(&tfull[0]);
+    }
+  } else if (warp < 6) {
+    const int q = warp & 3;
+    const int rowl = q * 32 + lane;
+    if (n_iter > 0) {
+      ptx::mbar_wait(&tfull[0], 0);
+      ptx::tc_fence_after();
+    }
+    for (int j = 0; j < g_cnt; ++j) {
+      const int rg = r0 + j * 128 + rowl;
+      for (int ch = 0; ch < a.BNw / 16; ++ch) {
+        float v[16];
+        if (n_iter > 0) {
+          ptx::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + j * a.BNw + ch * 16, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (rg < a.rows) {
+          float4* op = reinterpret_cast<float4*>(a.part + ((int64_t)ks * a.rows + rg) * a.Coutp + nt * a.BNw + ch * 16);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+    }
+  } else {
+    // converter: raw band / raw dY -> K-major hi/lo operands (4 rows x 4 pixels per unit)
+    const int ct = threadIdx.x - kBaseThreads;
+    const int hw = a.bh * a.Wo;
+    const int nq = a.P8 / 4;
+    const int unitsA = (g_cnt * 128 / 4) * nq;
+    const int unitsD = (a.BNw / 4) * nq;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int it = 0; it < n_iter; ++it) {
+      ptx::mbar_wait(&full[st], ph);
+      uint8_t* s0 = ring + st * a.stage_bytes;
+      const uint8_t* rawx = s0;
+      const uint8_t* rawd = s0 + off_rawd;
+      uint8_t* ahi = s0 + off_a;
+      uint8_t* alo = ahi + a.a_bytes;
+      uint8_t* dhi = s0 + off_d;
+      uint8_t* dlo = dhi + a.d_bytes;
+      for (int u = ct; u < unitsA + unitsD; u += 128) {
+        const bool isA = u < unitsA;
+        const int uu = isA ? u : u - unitsA;
+        const int q4 = uu / nq, pq = uu % nq;
+        float4 v[4];
+        if (isA) {
+          const int R = r0 + 4 * q4;
+          const int tap = R / a.Cinp, ci = R % a.Cinp;
+          const int r = tap / a.k, s = tap % a.k;
+          const int plane = ci / kEPC - pl0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int p = 4 * pq + i;
+            v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (R < r_end && p < a.P) {
+              const int jj = p / hw, py = (p / a.Wo) % a.bh, px = p % a.Wo;
+              const int off = ((plane * a.nb + jj) * a.band_r + py * a.S + r) * a.band_c + px * a.S + s;
+              v[i] = *reinterpret_cast<const float4*>(rawx + off * 16);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int p = 4 * pq + i;
+            v[i] = p < a.P ? *reinterpret_cast<const float4*>(rawd + (q4 * a.P + p) * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        uint8_t* hi = isA ? ahi : dhi;
+        uint8_t* lo = isA ? alo : dlo;
+        const float* f = reinterpret_cast<const float*>(v);   // f[px*4 + ch]
+#pragma unroll
+        for (int cl = 0; cl < 4; ++cl) {
+          const int rr = 4 * q4 + cl;
+          const uint32_t off = (uint32_t)((rr >> 3) * a.sbo + pq * 128 + (rr & 7) * 16);
+          const float4 h = make_float4(f[cl], f[4 + cl], f[8 + cl], f[12 + cl]);
+          *reinterpret_cast<float4*>(hi + off) = h;
+          *reinterpret_cast<float4*>(lo + off) = make_float4(tf32_lo(h.x), tf32_lo(h.y), tf32_lo(h.z), tf32_lo(h.w));
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&ready[st]);
+      if (++st == a.stages) { st = 0; ph ^= 1; }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, a.tmem_cols);
+  }
+}
+
 // largest multiple of 16 that divides C and is <= cap (C a multiple of 16)
 int tile_n(int C, int cap) {
   int best = 16;
@@ -560,22 +784,41 @@ void pixel_tile(int N, int Ho, int Wo, int npx, int& bimg, int& bh, int& bw) {
   bimg = npx / (bw * bh);
 }
 
-// activation tensor map: dims (EPC, Cp/EPC, W, H, N), box (EPC, 1, bw*S, bh*S, bimg)
-CUtensorMap act_tmap(const act_t* p, int N, int H, int W, int Cp, int bimg, int bh, int bw, int S) {
-  const uint64_t es = sizeof(act_t);
-  uint64_t dims[5] = {(uint64_t)kEPC, (uint64_t)Cp / kEPC, (uint64_t)W, (uint64_t)H, (uint64_t)N};
-  uint64_t str[4] = {16, (uint64_t)Cp * es, (uint64_t)W * Cp * es, (uint64_t)H * W * Cp * es};
-  uint32_t box[5] = {(uint32_t)kEPC, 1, (uint32_t)(bw * S), (uint32_t)(bh * S), (uint32_t)bimg};
-  uint32_t est[5] = {1, 1, (uint32_t)S, (uint32_t)S, 1};
+// channel-planar activation map.  smem receives [plane][img][y][x][16 B]: nch K-major
+// core-matrix columns of 128 pixel rows.
+//  stride 1: dims (W*EPC, H, N, Cp/EPC), box (bw*EPC, bh, bimg, nch) -- the innermost box
+//            extent is a whole run of bw pixels (bw*16 bytes), so TMA moves long rows;
+//            x coordinates are in elements (x*EPC).
+//  stride 2: dims (EPC, W, H, N, Cp/EPC) with element strides (1, 2, 2, 1, 1).
+CUtensorMap act_tmap(const act_t* p, int N, int H, int W, int Cp, int bimg, int bh, int bw, int S, int nch) {
+  if (S == 1 && bw * kEPC <= 256) {
+    uint64_t dims[4] = {(uint64_t)W * kEPC, (uint64_t)H, (uint64_t)N, (uint64_t)Cp / kEPC};
+    uint64_t str[3] = {(uint64_t)W * 16, (uint64_t)H * W * 16, (uint64_t)N * H * W * 16};
+    uint32_t box[4] = {(uint32_t)(bw * kEPC), (uint32_t)bh, (uint32_t)bimg, (uint32_t)nch};
+    return make_tmap(act_tmap_dtype(), 4, p, dims, str, box, nullptr);
+  }
+  uint64_t dims[5] = {(uint64_t)kEPC, (uint64_t)W, (uint64_t)H, (uint64_t)N, (uint64_t)Cp / kEPC};
+  uint64_t str[4] = {16, (uint64_t)W * 16, (uint64_t)H * W * 16, (uint64_t)N * H * W * 16};
+  uint32_t box[5] = {(uint32_t)kEPC, (uint32_t)(bw * S), (uint32_t)(bh * S), (uint32_t)bimg, (uint32_t)nch};
+  uint32_t est[5] = {1, (uint32_t)S, (uint32_t)S, 1, 1};
   return make_tmap(act_tmap_dtype(), 5, p, dims, str, box, est);
 }
+inline bool act_tmap_is4d(int S, int bw) { return S == 1 && bw * kEPC <= 256; }
 
-// weight shadow map: dims (EPC, Cinp/EPC, Coutp, taps), box (EPC, 1, BN, 1)
-CUtensorMap w_tmap(const act_t* p, int taps, int Coutp, int Cinp, int BN) {
-  const uint64_t es = sizeof(act_t);
-  uint64_t wd[4] = {(uint64_t)kEPC, (uint64_t)Cinp / kEPC, (uint64_t)Coutp, (uint64_t)taps};
-  uint64_t ws[3] = {16, (uint64_t)Cinp * es, (uint64_t)Coutp * Cinp * es};
-  uint32_t wb[4] = {(uint32_t)kEPC, 1, (uint32_t)BN, 1};
+// weight shadow map over [taps][Cinp/EPC][Coutp][EPC]; smem receives [plane][BN rows][16 B].
+//  BN*EPC <= 256: dims (Coutp*EPC, Cinp/EPC, taps), box (BN*EPC, nch, 1) -- long rows;
+//  else         : dims (EPC, Coutp, Cinp/EPC, taps), box (EPC, BN, nch, 1).
+inline bool w_tmap_is3d(int BN) { return BN * kEPC <= 256; }
+CUtensorMap w_tmap(const act_t* p, int taps, int Coutp, int Cinp, int BN, int nch) {
+  if (w_tmap_is3d(BN)) {
+    uint64_t wd[3] = {(uint64_t)Coutp * kEPC, (uint64_t)Cinp / kEPC, (uint64_t)taps};
+    uint64_t ws[2] = {(uint64_t)Coutp * 16, (uint64_t)Coutp * Cinp * sizeof(act_t)};
+    uint32_t wb[3] = {(uint32_t)(BN * kEPC), (uint32_t)nch, 1};
+    return make_tmap(act_tmap_dtype(), 3, p, wd, ws, wb, nullptr);
+  }
+  uint64_t wd[4] = {(uint64_t)kEPC, (uint64_t)Coutp, (uint64_t)Cinp / kEPC, (uint64_t)taps};
+  uint64_t ws[3] = {16, (uint64_t)Coutp * 16, (uint64_t)Coutp * Cinp * sizeof(act_t)};
+  uint32_t wb[4] = {(uint32_t)kEPC, (uint32_t)BN, (uint32_t)nch, 1};
   return make_tmap(act_tmap_dtype(), 4, p, wd, ws, wb, nullptr);
 }
 
@@ -623,10 +866,12 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
   a.res = c.res; a.res_mode = c.res_mode; a.res_H = c.res_H; a.res_W = c.res_W; a.res_C = c.res_C;
   a.res_pad = c.res_pad;
 
-  CUtensorMap tA = act_tmap(c.in, c.N, c.H, c.W, c.Cinp, a.bimg, a.bh, a.bw, c.S);
-  CUtensorMap tB = w_tmap(c.wshadow, a.taps, c.Coutp, c.Cinp, a.BN);
-  CUtensorMap tBlo = PST_SPLIT ? w_tmap(c.wshadow + (size_t)a.taps * c.Coutp * c.Cinp, a.taps, c.Coutp, c.Cinp, a.BN)
-                               : tB;
+  a.a4 = act_tmap_is4d(c.S, a.bw) ? 1 : 0;
+  a.b3 = w_tmap_is3d(a.BN) ? 1 : 0;
+  CUtensorMap tA = act_tmap(c.in, c.N, c.H, c.W, c.Cinp, a.bimg, a.bh, a.bw, c.S, nch);
+  CUtensorMap tB = w_tmap(c.wshadow, a.taps, c.Coutp, c.Cinp, a.BN, nch);
+  CUtensorMap tBlo =
+      PST_SPLIT ? w_tmap(c.wshadow + (size_t)a.taps * c.Coutp * c.Cinp, a.taps, c.Coutp, c.Cinp, a.BN, nch) : tB;
   const size_t smem = (size_t)a.stages * a.stage_bytes + (16 * 129 + 4) * 4 + 2 * c.Coutp * 8 +
                       (3 * kMaxStages + 4) * 8 + 16;
   PST_CHECK_ARG(smem <= 227 * 1024, "conv smem budget");
@@ -646,7 +891,68 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
   prof::end(st, c.epi == EPI_DGRAD ? prof::CONV_DGRAD : prof::CONV_FWD, bytes, flops);
 }
 
-WgradPlan wgrad_plan(int N, int Ho, int Wo, int Cinp, int Coutp, int k, int num_sm) {
+// Stage geometry, M grouping, smem layout and split-K factor of conv_wgrad_band_kernel.
+WbArgs plan_band(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm) {
+  WbArgs a{};
+  a.N = N; a.H = H; a.W = W; a.Cinp = Cinp; a.Ho = Ho; a.Wo = Wo; a.Coutp = Coutp;
+  a.k = k; a.S = S; a.pad = pad;
+  a.rows = k * k * Cinp;
+  a.n_mt = ceil_div(a.rows, 128);
+  a.BNw = tile_n(Coutp, 128);
+  a.n_ntiles = Coutp / a.BNw;
+  const int budget = 200 * 1024;
+  for (int ptarget : {32, 16, 8}) {
+    if (Ho * Wo >= ptarget) { a.nb = 1; a.bh = std::max(1, std::min(Ho, ptarget / Wo)); }
+    else { a.nb = std::max(1, std::min(N, ptarget / (Ho * Wo))); a.bh = Ho; }
+    a.P = a.nb * a.bh * Wo;
+    a.P8 = round_up(a.P, 8);
+    a.band_r = (a.bh - 1) * S + k;
+    a.band_c = (Wo - 1) * S + k;
+    bool ok = false;
+    for (int G = std::min(a.n_mt, std::max(1, 512 / a.BNw)); G >= 1; --G) {
+      const bool all = (G * 128 >= Cinp) || (Cinp % (G * 128) != 0);
+      const int pl = all ? Cinp / kEPC : G * 128 / kEPC;
+      const uint32_t rawx = (uint32_t)pl * a.nb * a.band_r * a.band_c * 16;
+      const uint32_t rawd = (uint32_t)(a.BNw / kEPC) * a.P * 16;
+      const uint32_t ab = (uint32_t)G * 128 * a.P8 * 4, db = (uint32_t)a.BNw * a.P8 * 4;
+      const uint32_t stage = round_up((int)(rawx + rawd), 128) + 2 * ab + 2 * db;
+      const bool units_ok = (G * 128 / 4 + a.BNw / 4) * (a.P8 / 4) <= 128 * 64;
+      if (a.band_c * kEPC <= 256 && units_ok && 2 * stage <= (uint32_t)budget) {
+        a.G = G; a.pl_all = all ? 1 : 0; a.pl_grp = pl;
+        a.rawx_bytes = round_up((int)rawx, 128); a.rawx_tx = rawx; a.rawd_bytes = rawd;
+        a.a_bytes = ab; a.d_bytes = db; a.stage_bytes = a.rawx_bytes + rawd + 2 * ab + 2 * db;
+        ok = true;
+        break;
+      }
+    }
+    if (ok) break;
+  }
+  if (a.G < 1) return a;   // infeasible (huge input bands): caller falls back to per-tap loads
+  a.stage_bytes = round_up((int)a.stage_bytes, 1024);
+  a.stages = std::max(1, std::min(4, budget / (int)a.stage_bytes));
+  a.sbo = (uint32_t)(a.P8 / 4) * 128;
+  a.n_mgroups = ceil_div(a.n_mt, a.G);
+  a.ny = ceil_div(Ho, a.bh);
+  a.n_units = ceil_div(N, a.nb) * a.ny;
+  const int base = a.n_mgroups * a.n_ntiles;
+  a.ksplit = std::max(1, std::min(std::max(1, a.n_units / 2), num_sm / base));
+  a.tmem_cols = (uint32_t)std::max(32, pow2_at_least(a.G * a.BNw));
+  return a;
+}
+
+WgradPlan wgrad_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm) {
+#if PST_SPLIT
+  {
+    const WbArgs b = plan_band(N, H, W, Cinp, Ho, Wo, Coutp, k, S, pad, num_sm);
+    if (b.G >= 1) {
+      WgradPlan p;
+      p.ksplit = b.ksplit;
+      p.part_floats = (int64_t)b.ksplit * b.rows * Coutp;
+      return p;
+    }
+  }
+#endif
+  (void)H; (void)W; (void)S; (void)pad;
   int bimg, bh, bw;
   pixel_tile(N, Ho, Wo, kWgPix, bimg, bh, bw);
   const int n_ptiles = ceil_div(N, bimg) * ceil_div(Ho, bh) * ceil_div(Wo, bw);
@@ -667,6 +973,38 @@ WgradPlan wgrad_plan(int N, int Ho, int Wo, int Cinp, int Coutp, int k, int num_
 
 void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
   PST_CHECK_ARG(w.Cinp % 16 == 0 && w.Coutp % 16 == 0, "wgrad channels must be padded to 16");
+#if PST_SPLIT
+  int dev_b;
+  PST_CUDA(cudaGetDevice(&dev_b));
+  WbArgs b = plan_band(w.N, w.H, w.W, w.Cinp, w.Ho, w.Wo, w.Coutp, w.k, w.S, w.pad, num_sms(dev_b));
+  if (b.G >= 1) {
+    PST_CHECK_ARG(b.ksplit == w.ksplit, "wgrad: workspace planned for a different split");
+    b.part = w.part;
+    // X: dims (W*EPC, H, N, Cinp/EPC), box (band_c*EPC, band_r, nb, pl_grp)
+    uint64_t xd[4] = {(uint64_t)w.W * kEPC, (uint64_t)w.H, (uint64_t)w.N, (uint64_t)w.Cinp / kEPC};
+    uint64_t xs[3] = {(uint64_t)w.W * 16, (uint64_t)w.H * w.W * 16, (uint64_t)w.N * w.H * w.W * 16};
+    uint32_t xb[4] = {(uint32_t)(b.band_c * kEPC), (uint32_t)b.band_r, (uint32_t)b.nb, (uint32_t)b.pl_grp};
+    CUtensorMap tX = make_tmap(act_tmap_dtype(), 4, w.x, xd, xs, xb, nullptr);
+    // dY: dims (Wo*EPC, Ho, N, Coutp/EPC), box (Wo*EPC, bh, nb, BNw/EPC)
+    uint64_t dd[4] = {(uint64_t)w.Wo * kEPC, (uint64_t)w.Ho, (uint64_t)w.N, (uint64_t)w.Coutp / kEPC};
+    uint64_t ds[3] = {(uint64_t)w.Wo * 16, (uint64_t)w.Ho * w.Wo * 16, (uint64_t)w.N * w.Ho * w.Wo * 16};
+    uint32_t db[4] = {(uint32_t)(w.Wo * kEPC), (uint32_t)b.bh, (uint32_t)b.nb, (uint32_t)(b.BNw / kEPC)};
+    CUtensorMap tD = make_tmap(act_tmap_dtype(), 4, w.dy, dd, ds, db, nullptr);
+    const size_t smem = (size_t)b.stages * b.stage_bytes + (3 * kMaxStages + 2) * 8 + 16;
+    PST_CHECK_ARG(smem <= 227 * 1024, "wgrad smem budget");
+    PST_CUDA(cudaFuncSetAttribute(conv_wgrad_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = b.n_mgroups * b.n_ntiles * b.ksplit;
+    const double es = sizeof(act_t);
+    const double bytes = (double)w.N * w.H * w.W * w.Cinp * es + (double)w.N * w.Ho * w.Wo * w.Coutp * es +
+                         (double)b.ksplit * b.rows * w.Coutp * 4.0;
+    const double flops = 2.0 * b.rows * (double)w.Coutp * w.N * w.Ho * w.Wo;
+    prof::begin(st);
+    conv_wgrad_band_kernel<<<grid, kThreads, smem, st>>>(tX, tD, b);
+    PST_CUDA(cudaGetLastError());
+    prof::end(st, prof::CONV_WGRAD, bytes, flops);
+    return;
+  }
+#endif
   WgArgs a{};
   a.N = w.N; a.Ho = w.Ho; a.Wo = w.Wo;
   pixel_tile(w.N, w.Ho, w.Wo, kWgPix, a.bimg, a.bh, a.bw);
@@ -690,8 +1028,10 @@ void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
   a.tmem_cols = (uint32_t)std::max(32, pow2_at_least(a.G * a.BNw));
   a.part = w.part;
 
-  CUtensorMap tX = act_tmap(w.x, w.N, w.H, w.W, w.Cinp, a.bimg, a.bh, a.bw, w.S);
-  CUtensorMap tD = act_tmap(w.dy, w.N, w.Ho, w.Wo, w.Coutp, a.bimg, a.bh, a.bw, 1);
+  a.x4 = act_tmap_is4d(w.S, a.bw) ? 1 : 0;
+  a.d4 = act_tmap_is4d(1, a.bw) ? 1 : 0;
+  CUtensorMap tX = act_tmap(w.x, w.N, w.H, w.W, w.Cinp, a.bimg, a.bh, a.bw, w.S, 1);
+  CUtensorMap tD = act_tmap(w.dy, w.N, w.Ho, w.Wo, w.Coutp, a.bimg, a.bh, a.bw, 1, a.BNw / kEPC);
   PST_CUDA(cudaFuncSetAttribute(conv_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = a.n_mgroups * a.n_ntiles * a.ksplit;
   const double es = sizeof(act_t);

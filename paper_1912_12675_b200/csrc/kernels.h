@@ -1,10 +1,15 @@
 // kernels.h -- launch interfaces of the hand-written sm_100a kernels of libpst.
 //
 // Layouts:
-//   activations / gradients : NHWC act_t, channels padded to Cp = round_up(C, 16)
-//   conv weight shadows     : fwd   [k*k][Coutp][Cinp] act_t  (K-major B operand)
-//                             dgrad [k*k][Cinp][Coutp] act_t  (taps applied flipped)
-//   master weights          : canonical float32 (OIHW / [out][in]) per stage
+//   activations / gradients : channel-planar act_t [Cp/EPC][N][H][W][EPC], channels padded
+//                             to Cp = round_up(C, 16), EPC = 16 B / sizeof(act_t); a TMA box
+//                             row is then a contiguous run of pixels of one 16-byte plane.
+//   float tensors (logits, loss gradient): [Cp/4][N][H][W][4]
+//   conv weight shadows     : fwd   [k*k][Cinp/EPC][Coutp][EPC]  (K-major B operand rows)
+//                             dgrad [k*k][Coutp/EPC][Cinp][EPC]
+//                             3xTF32 build: a lo plane (w - trunc_tf32(w)) follows each.
+//   master weights          : canonical float32 (OIHW; an FC layer over a CxHxW tensor is
+//                             the valid convolution with k = H = W) per stage
 #pragma once
 #include "common.h"
 
@@ -42,12 +47,12 @@ struct WgradSpec {
   int ksplit;               // chosen by wgrad_plan
 };
 struct WgradPlan { int ksplit; int64_t part_floats; };
-WgradPlan wgrad_plan(int N, int Ho, int Wo, int Cinp, int Coutp, int k, int num_sm);
+WgradPlan wgrad_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm);
 void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st);
 
 // ---------------------------------------------------------------- elementwise / reductions
-// NCHW float32 -> NHWC act_t, channels zero-padded to Cp.
-void input_to_nhwc(const float* x, act_t* out, int N, int C, int H, int W, int Cp, cudaStream_t st);
+// NCHW float32 -> channel-planar act_t, channels zero-padded to Cp.
+void input_to_act(const float* x, act_t* out, int N, int C, int H, int W, int Cp, cudaStream_t st);
 
 // BN forward apply (train mode): batch stats from `stats` (sum, sumsq over M values),
 // z = relu?( gamma*(y-mean)*invstd + beta + shortcut(block) ).  Block 0 also writes
@@ -112,15 +117,14 @@ void softmax_ce(const float* logits, const int32_t* label_ring, int ring, float*
 // v = mu v + (g + lambda w), w -= lr v, plus the act_t weight shadows.
 // lr = (v_count < n_p ? lr_pipe : lr_np) * gamma^(#milestones <= v_count/spe);
 // the kernel reads and then increments *v_count.
-enum SegKind { SEG_CONVW = 0, SEG_FCW = 1, SEG_VEC = 2 };
+enum SegKind { SEG_CONVW = 0, SEG_VEC = 2 };
 struct SgdSeg {
   int kind;
   int64_t off;              // canonical offset in the stage's flat parameter vector
   int64_t n;                // elements
-  // SEG_CONVW / SEG_FCW
-  int cout, cin, k;         // canonical dims (FC: k = 1)
-  int Coutp, Cinp;          // padded GEMM dims (FC: Cinp = H*W*Cp_in)
-  int fc_C, fc_H, fc_W, fc_Cp;  // FC input tensor geometry for the NCHW-flatten mapping
+  // SEG_CONVW (an FC layer over a CxHxW input is the valid conv with k = H)
+  int cout, cin, k;         // canonical dims
+  int Coutp, Cinp;          // padded GEMM dims
   const float* part; int ksplit;  // wgrad partials [ksplit][k*k*Cinp][Coutp]
   act_t* sh_fwd;            // [k*k][Coutp][Cinp]
   act_t* sh_bwd;            // [k*k][Cinp][Coutp]
@@ -148,7 +152,7 @@ void build_shadows(const SgdSpec& s, cudaStream_t st);
 
 namespace pst {
 // ---------------------------------------------------------------- test/debug helpers (ops ABI)
-void nhwc_to_nchw(const void* in, int in_f32, float* out, int N, int C, int H, int W, int Cp, cudaStream_t st);
+void act_to_nchw(const void* in, int in_f32, float* out, int N, int C, int H, int W, cudaStream_t st);
 void conv_weights_to_shadows(const float* w, int cout, int cin, int k, int Coutp, int Cinp, act_t* sh_fwd,
                              act_t* sh_bwd, cudaStream_t st);
 void wgrad_reduce(const float* part, int ksplit, int Coutp, int Cinp, int cout, int cin, int k, float* out,

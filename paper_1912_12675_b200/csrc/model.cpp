@@ -34,6 +34,7 @@ NetInfo derive_net(const pst_net& net) {
       PST_CHECK_ARG(L.k >= 1 && L.k <= 7 && L.pad >= 0 && L.pad < L.k, at + "conv k/pad");
       PST_CHECK_ARG(L.stride == 1 || L.stride == 2, at + "stride must be 1 or 2");
       li.Cinp = li.in_Cp;
+      li.kk = L.k; li.S = L.stride; li.pad = L.pad;
       li.Ho = (H + 2 * L.pad - L.k) / L.stride + 1;
       li.Wo = (W + 2 * L.pad - L.k) / L.stride + 1;
       PST_CHECK_ARG(li.Ho >= 1 && li.Wo >= 1, at + "empty conv output");
@@ -41,7 +42,9 @@ NetInfo derive_net(const pst_net& net) {
         PST_CHECK_ARG(L.k == 3 && L.pad == 1, at + "stride-2 conv supported for k=3, pad=1");
     } else if (L.kind == PST_LAYER_FC) {
       PST_CHECK_ARG(L.cin == C * H * W, at + "FC cin must equal C*H*W of the incoming tensor");
-      li.Cinp = H * W * li.in_Cp;
+      PST_CHECK_ARG(H == W && H <= 7, at + "FC input must be square with H <= 7 (valid-conv view)");
+      li.Cinp = li.in_Cp;
+      li.kk = H; li.S = 1; li.pad = 0;
       li.Ho = li.Wo = 1;
     } else {
       throw InvalidArg(at + "unknown layer kind");

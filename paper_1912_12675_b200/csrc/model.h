@@ -15,8 +15,11 @@ struct LayerInfo {
   int idx = 0;
   // input tensor (NCHW geometry of what arrives; for FC the pre-flatten tensor)
   int in_C = 0, in_H = 0, in_W = 0, in_Cp = 0;
-  // GEMM view: K channels per tap and spatial of the conv output (pre-pool)
-  int Cinp = 0;             // conv: in_Cp; FC: in_H*in_W*in_Cp
+  // GEMM view: every weighted layer is a convolution over the input tensor; an FC
+  // layer over a CxHxW tensor is the valid convolution with kk = H = W (its
+  // canonical [out][c*H*W + y*W + x] weights are exactly OIHW).
+  int kk = 1, S = 1, pad = 0;
+  int Cinp = 0;             // K channels per tap = in_Cp
   int Ho = 0, Wo = 0;       // conv output spatial (FC: 1x1)
   int Coutp = 0;            // padded output channels
   // the layer's output tensor (after pool): next layer's input

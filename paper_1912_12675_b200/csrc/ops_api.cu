@@ -60,7 +60,7 @@ int pst_op_conv2d_fwd(const float* x, const float* w, float* y, int N, int Cin, 
     act_t* sf = s.get<act_t>((size_t)k * k * g.Coutp * g.Cinp * (PST_SPLIT ? 2 : 1));
     act_t* sb = s.get<act_t>((size_t)k * k * g.Coutp * g.Cinp * (PST_SPLIT ? 2 : 1));
     float* yo = s.get<float>((size_t)N * g.Ho * g.Wo * g.Coutp);
-    input_to_nhwc(x, xa, N, Cin, H, W, g.Cinp, 0);
+    input_to_act(x, xa, N, Cin, H, W, g.Cinp, 0);
     conv_weights_to_shadows(w, Cout, Cin, k, g.Coutp, g.Cinp, sf, sb, 0);
     ConvSpec c{};
     c.in = xa; c.N = N; c.H = H; c.W = W; c.Cinp = g.Cinp;
@@ -68,7 +68,7 @@ int pst_op_conv2d_fwd(const float* x, const float* w, float* y, int N, int Cin, 
     c.k = k; c.S = stride; c.off = -pad; c.sgn = 1;
     c.wshadow = sf; c.epi = EPI_BIAS_F32; c.out = yo;
     conv_tc(c, 0);
-    nhwc_to_nchw(yo, 1, y, N, Cout, g.Ho, g.Wo, g.Coutp, 0);
+    act_to_nchw(yo, 1, y, N, Cout, g.Ho, g.Wo, 0);
     PST_CUDA(cudaDeviceSynchronize());
   });
 }
@@ -83,7 +83,7 @@ int pst_op_conv2d_dgrad(const float* gy, const float* w, float* gx, int N, int C
     act_t* sf = s.get<act_t>((size_t)k * k * g.Coutp * g.Cinp * (PST_SPLIT ? 2 : 1));
     act_t* sb = s.get<act_t>((size_t)k * k * g.Coutp * g.Cinp * (PST_SPLIT ? 2 : 1));
     act_t* gxa = s.get<act_t>((size_t)N * H * W * g.Cinp);
-    input_to_nhwc(gy, ga, N, Cout, g.Ho, g.Wo, g.Coutp, 0);
+    input_to_act(gy, ga, N, Cout, g.Ho, g.Wo, g.Coutp, 0);
     conv_weights_to_shadows(w, Cout, Cin, k, g.Coutp, g.Cinp, sf, sb, 0);
     const act_t* src = ga;
     int sH = g.Ho, sW = g.Wo;
@@ -98,7 +98,7 @@ int pst_op_conv2d_dgrad(const float* gy, const float* w, float* gx, int N, int C
     c.k = k; c.S = 1; c.off = pad; c.sgn = -1;
     c.wshadow = sb; c.epi = EPI_DGRAD; c.out = gxa;
     conv_tc(c, 0);
-    nhwc_to_nchw(gxa, 0, gx, N, Cin, H, W, g.Cinp, 0);
+    act_to_nchw(gxa, 0, gx, N, Cin, H, W, 0);
     PST_CUDA(cudaDeviceSynchronize());
   });
 }
@@ -110,11 +110,11 @@ int pst_op_conv2d_wgrad(const float* x, const float* gy, float* gw, int N, int C
     Scratch s;
     act_t* xa = s.get<act_t>((size_t)N * H * W * g.Cinp);
     act_t* ga = s.get<act_t>((size_t)N * g.Ho * g.Wo * g.Coutp);
-    input_to_nhwc(x, xa, N, Cin, H, W, g.Cinp, 0);
-    input_to_nhwc(gy, ga, N, Cout, g.Ho, g.Wo, g.Coutp, 0);
+    input_to_act(x, xa, N, Cin, H, W, g.Cinp, 0);
+    input_to_act(gy, ga, N, Cout, g.Ho, g.Wo, g.Coutp, 0);
     int dev;
     PST_CUDA(cudaGetDevice(&dev));
-    WgradPlan p = wgrad_plan(N, g.Ho, g.Wo, g.Cinp, g.Coutp, k, num_sms(dev));
+    WgradPlan p = wgrad_plan(N, H, W, g.Cinp, g.Ho, g.Wo, g.Coutp, k, stride, pad, num_sms(dev));
     float* part = s.get<float>((size_t)p.part_floats);
     WgradSpec wg{};
     wg.x = xa; wg.N = N; wg.H = H; wg.W = W; wg.Cinp = g.Cinp;

@@ -79,12 +79,10 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     if (li.spec.bn) b.gy = alloc<act_t>(out_el, false);
     const bool need_gin = !(is_first() && l == l0);
     if (need_gin) b.gin = alloc<act_t>((size_t)B * li.in_H * li.in_W * li.in_Cp, false);
-    if (li.spec.kind == PST_LAYER_CONV && li.spec.stride == 2 && need_gin)
+    if (li.S == 2 && need_gin)
       b.dil = alloc<act_t>((size_t)B * li.in_H * li.in_W * li.Coutp, false);
-    const int kk = li.spec.kind == PST_LAYER_CONV ? li.spec.k : 1;
-    const int wH = li.spec.kind == PST_LAYER_CONV ? li.in_H : 1;
-    WgradPlan wp = wgrad_plan(B, li.Ho, li.Wo, li.Cinp, li.Coutp, kk, nsm);
-    (void)wH;
+    const int kk = li.kk;
+    WgradPlan wp = wgrad_plan(B, li.in_H, li.in_W, li.Cinp, li.Ho, li.Wo, li.Coutp, kk, li.S, li.pad, nsm);
     b.ksplit = wp.ksplit;
     b.wpart = alloc<float>((size_t)wp.part_floats, false);
     // weight shadows (+ the 3xTF32 lo plane right after the raw plane in the split build)
@@ -129,14 +127,9 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     g.ksplit = b.ksplit;
     g.sh_fwd = b.sh_fwd;
     g.sh_bwd = b.sh_bwd;
-    if (li.spec.kind == PST_LAYER_CONV) {
-      g.kind = SEG_CONVW;
-      g.k = li.spec.k;
-    } else {
-      g.kind = SEG_FCW;
-      g.k = 1;
-      g.fc_C = li.in_C; g.fc_H = li.in_H; g.fc_W = li.in_W; g.fc_Cp = li.in_Cp;
-    }
+    g.kind = SEG_CONVW;   // FC over CxHxW = valid conv with k = H (canonical [o][c*H*W+y*W+x] == OIHW)
+    g.k = li.kk;
+    g.cin = li.in_C;
     add(g);
     if (li.spec.bias) {
       SgdSeg v{}; v.kind = SEG_VEC; v.off = li.off_b - p_base; v.n = li.spec.cout; v.src_d = b.sums; v.comp = 0;
@@ -223,23 +216,22 @@ void Stage::enqueue_forward(int slot, cudaStream_t st) {
   const int B = batch_;
   if (fwd_arena_n_) PST_CUDA(cudaMemsetAsync(fwd_arena_, 0, fwd_arena_n_ * sizeof(double), st));
   if (is_first())
-    input_to_nhwc(xstage_, xin_[slot], B, net_.in_C, net_.in_H, net_.in_W, net_.in_Cp, st);
+    input_to_act(xstage_, xin_[slot], B, net_.in_C, net_.in_H, net_.in_W, net_.in_Cp, st);
   int bn_local = 0;
   for (int l = l0; l < l1; ++l) {
     const LayerInfo& li = net_.layers[l];
     LayerBufs& b = L_[l - l0];
     const bool last_net = (l == (int)net_.layers.size() - 1);
-    const bool conv = li.spec.kind == PST_LAYER_CONV;
     ConvSpec c{};
     c.in = in_tensor(l, slot);
     c.N = B;
-    c.H = conv ? li.in_H : 1;
-    c.W = conv ? li.in_W : 1;
+    c.H = li.in_H;
+    c.W = li.in_W;
     c.Cinp = li.Cinp;
     c.Ho = li.Ho; c.Wo = li.Wo; c.Coutp = li.Coutp; c.Cout = li.spec.cout;
-    c.k = conv ? li.spec.k : 1;
-    c.S = conv ? li.spec.stride : 1;
-    c.off = conv ? -li.spec.pad : 0;
+    c.k = li.kk;
+    c.S = li.S;
+    c.off = -li.pad;
     c.sgn = 1;
     c.wshadow = b.sh_fwd;
     c.relu = li.spec.relu;
@@ -297,7 +289,6 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
     const LayerInfo& li = net_.layers[l];
     LayerBufs& b = L_[l - l0];
     const bool last_net = (l == (int)net_.layers.size() - 1);
-    const bool conv = li.spec.kind == PST_LAYER_CONV;
     BwdPreSpec pr{};
     if (last_net) {
       pr.gout = reinterpret_cast<const act_t*>(dz_);
@@ -332,13 +323,13 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
     WgradSpec wg{};
     wg.x = in_tensor(l, slot);
     wg.N = B;
-    wg.H = conv ? li.in_H : 1;
-    wg.W = conv ? li.in_W : 1;
+    wg.H = li.in_H;
+    wg.W = li.in_W;
     wg.Cinp = li.Cinp;
     wg.dy = dY; wg.Ho = li.Ho; wg.Wo = li.Wo; wg.Coutp = li.Coutp;
-    wg.k = conv ? li.spec.k : 1;
-    wg.S = conv ? li.spec.stride : 1;
-    wg.pad = conv ? li.spec.pad : 0;
+    wg.k = li.kk;
+    wg.S = li.S;
+    wg.pad = li.pad;
     wg.part = b.wpart;
     wg.ksplit = b.ksplit;
     conv_wgrad_tc(wg, st);
@@ -347,19 +338,19 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
       ConvSpec c{};
       const act_t* src = dY;
       int sH = li.Ho, sW = li.Wo;
-      if (conv && li.spec.stride == 2) {
+      if (li.S == 2) {
         dilate2(dY, b.dil, B, li.Ho, li.Wo, li.in_H, li.in_W, li.Coutp, st);
         src = b.dil; sH = li.in_H; sW = li.in_W;
       }
       c.in = src; c.N = B;
-      c.H = conv ? sH : 1; c.W = conv ? sW : 1;
+      c.H = sH; c.W = sW;
       c.Cinp = li.Coutp;
-      c.Ho = conv ? li.in_H : 1; c.Wo = conv ? li.in_W : 1;
+      c.Ho = li.in_H; c.Wo = li.in_W;
       c.Coutp = li.Cinp;
-      c.Cout = conv ? li.in_C : li.Cinp;
-      c.k = conv ? li.spec.k : 1;
+      c.Cout = li.in_C;
+      c.k = li.kk;
       c.S = 1;
-      c.off = conv ? li.spec.pad : 0;
+      c.off = li.pad;
       c.sgn = -1;
       c.wshadow = b.sh_bwd;
       c.epi = EPI_DGRAD;
