@@ -27,6 +27,7 @@
 #include "ptx.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace pst {
 
@@ -54,6 +55,12 @@ struct FwdArgs {
   const act_t* res;
   int res_mode, res_H, res_W, res_C, res_pad;
   int a4, b3;   // tensor-map forms (act_tmap / w_tmap)
+  // HALO mode: virtual-grid pitch, lowest tap offset, tiles per image, band plane bytes,
+  // resident weight bytes (0: per stage), stage B bytes, per-tap start offsets (positions)
+  int Wv, lo, tpi, MT, Pimg;   // Pimg = Ho*Wv positions per image; MT M-tiles per super tile
+  uint32_t plane_bytes, wres_bytes, sb_bytes;
+  int tapoff[49];
+  unsigned long long* dbg;   // optional timeline (CTA 0), see PST_DBG_TL
 };
 
 __device__ __forceinline__ void decode_tile_px(const FwdArgs& a, int mt, int row, int& n, int& y,
@@ -120,14 +127,38 @@ __device__ __forceinline__ void tma_w(void* dst, const CUtensorMap* tm, uint64_t
   }
 }
 
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// timeline probe (debug only): event ev, occurrence i, CTA 0
+#define TL(ev, i)                                                                  \
+  do {                                                                             \
+    if (a.dbg != nullptr && blockIdx.x == 0) {                                     \
+      const int i_ = (i);                                                          \
+      if (i_ < 256) a.dbg[(ev) * 256 + i_] = gtime();                              \
+    }                                                                              \
+  } while (0)
+
+// HALO (stride-1 layers, Wo >= 16): the M tile is 128 consecutive positions of a
+// "virtual" output grid of row pitch Wv = Wo + k - 1 inside one image (positions with
+// x >= Wo are computed and discarded).  One TMA box loads the input band those
+// positions read for EVERY tap; tap (oy, ox) is then just the band shifted by
+// (oy-lo)*Wv + (ox-lo) positions -- a descriptor start offset, no re-load.  Weights of
+// all taps stay resident in smem when they fit.
+template <bool HALO>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmBlo, const FwdArgs a) {
+  int dbg_i[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (threadIdx.x == 0) TL(7, 0);
   extern __shared__ __align__(1024) uint8_t smem[];
-  // [stages x stage_bytes] [sbuf 16x129 f32] [acc doubles 2*Coutp] [barriers] [tmem ptr]
-  // stage: [A raw][B raw]([A lo][B lo] in the split build)
+  // [stages x stage_bytes] [resident weights (HALO && wres)] [sbuf 16x129 f32] [acc doubles 2*Coutp]
+  // [barriers] [tmem ptr];  stage: [A raw][B raw]([A lo][B lo] in the split build)
   uint8_t* ring = smem;
-  float* sbuf = reinterpret_cast<float*>(smem + a.stages * a.stage_bytes);
+  uint8_t* wres = smem + a.stages * a.stage_bytes;
+  float* sbuf = reinterpret_cast<float*>(wres + a.wres_bytes);
   double* cacc = reinterpret_cast<double*>(sbuf + 16 * 129 + 4);
   uint64_t* bars = reinterpret_cast<uint64_t*>(cacc + 2 * a.Coutp);
   uint64_t* full = bars;
@@ -135,7 +166,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* ready = bars + 2 * kMaxStages;
   uint64_t* tfull = bars + 3 * kMaxStages;
   uint64_t* tempty = bars + 3 * kMaxStages + 2;
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 4);
+  uint64_t* wbar = bars + 3 * kMaxStages + 4;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 5);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -150,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], 4);
     }
+    ptx::mbar_init(wbar, 1);
     ptx::fence_mbar_init();
   }
   if (a.epi == EPI_BN_STATS)
@@ -169,14 +202,45 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (PST_SPLIT) ptx::prefetch_tmap(&tmBlo);
       int st = 0;
       uint32_t ph = 0;
+      if (HALO && a.wres_bytes) {   // resident weights: every chunk, every tap (+lo), once per CTA
+        ptx::mbar_expect_tx(wbar, a.wres_bytes);
+        for (int kcc = 0; kcc < a.n_kc; ++kcc) {
+          tma_w(wres + kcc * a.b_bytes, &tmB, wbar, a.b3, 0, kcc * nch, 0);
+#if PST_SPLIT
+          tma_w(wres + (a.n_kc + kcc) * a.b_bytes, &tmBlo, wbar, a.b3, 0, kcc * nch, 0);
+#endif
+        }
+      }
       for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
         const int mt = t / a.n_ntiles, nt = t % a.n_ntiles;
+        if (HALO) {
+          const int n = mt / a.tpi, g0 = (mt % a.tpi) * 128 * a.MT;
+          const int yf = g0 / a.Wv;
+          for (int kcc = 0; kcc < a.n_kc; ++kcc) {
+            ptx::mbar_wait(&empty[st], ph ^ 1);
+            TL(0, dbg_i[0]++);
+            ptx::mbar_expect_tx(&full[st], a.tx_bytes);
+            uint8_t* sa = ring + st * a.stage_bytes;
+            for (int cx = 0; cx < a.k; ++cx)   // k column-shifted copies: every tap start is 128-B aligned
+              tma_act(sa + cx * nch * a.plane_bytes, &tmA, &full[st], true, a.lo + cx, yf + a.lo, n, kcc * nch);
+            if (!a.wres_bytes) {
+              uint8_t* sb = sa + a.a_bytes;
+              tma_w(sb, &tmB, &full[st], a.b3, nt * a.BN, kcc * nch, 0);
+#if PST_SPLIT
+              tma_w(sb + a.a_bytes + a.sb_bytes, &tmBlo, &full[st], a.b3, nt * a.BN, kcc * nch, 0);
+#endif
+            }
+            if (++st == a.stages) { st = 0; ph ^= 1; }
+          }
+          continue;
+        }
         const int ix = mt % a.tx, iy = (mt / a.tx) % a.ty, it = mt / (a.tx * a.ty);
         const int x0 = ix * a.bw * a.S + a.off, y0 = iy * a.bh * a.S + a.off, n0 = it * a.bimg;
         for (int tap = 0; tap < a.taps; ++tap) {
           const int r = tap / a.k, s = tap % a.k;
           for (int kcc = 0; kcc < a.n_kc; ++kcc) {
             ptx::mbar_wait(&empty[st], ph ^ 1);
+            TL(0, dbg_i[0]++);
             ptx::mbar_expect_tx(&full[st], a.tx_bytes);
             uint8_t* sa = ring + st * a.stage_bytes;
             uint8_t* sb = sa + a.a_bytes;
@@ -185,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_act(sa, &tmA, &full[st], a.a4, x0 + a.sgn * s, y0 + a.sgn * r, n0, cc);
             tma_w(sb, &tmB, &full[st], a.b3, nt * a.BN, cc, tap);
 #if PST_SPLIT
-            tma_w(sb + a.a_bytes + a.b_bytes, &tmBlo, &full[st], a.b3, nt * a.BN, cc, tap);
+            tma_w(sb + a.a_bytes + a.sb_bytes, &tmBlo, &full[st], a.b3, nt * a.BN, cc, tap);
 #endif
             if (++st == a.stages) { st = 0; ph ^= 1; }
           }
@@ -199,16 +263,63 @@ __global__ void __launch_bounds__(kThreads, 1)
       int st = 0;
       uint32_t ph = 0;
       int local = 0;
+      if (HALO && a.wres_bytes) ptx::mbar_wait(wbar, 0);
       for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++local) {
         const int acc = local & 1;
         const uint32_t use = (uint32_t)(local >> 1);
         ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
         ptx::tc_fence_after();
-        const uint32_t dtm = tmem_base + acc * a.BN;
+        const uint32_t dtm = tmem_base + acc * a.BN * (HALO ? a.MT : 1);
+        if (HALO) {
+          const int mt = t / a.n_ntiles;
+          const int g0 = (mt % a.tpi) * 128 * a.MT;
+          const int mtv = min(a.MT, (a.Pimg - g0 + 127) / 128);         // M tiles with valid rows
+          const uint32_t base_pos = (uint32_t)(g0 - (g0 / a.Wv) * a.Wv);   // g0 relative to its band row
+          for (int kcc = 0; kcc < a.n_kc; ++kcc) {
+            ptx::mbar_wait(PST_SPLIT ? &ready[st] : &full[st], ph);
+            TL(3, dbg_i[3]++);
+            ptx::tc_fence_after();
+            const uint32_t sa = ptx::smem_u32(ring + st * a.stage_bytes);
+            const uint32_t off_lo = a.a_bytes + a.sb_bytes;
+            const uint32_t wb = a.wres_bytes ? ptx::smem_u32(wres) + kcc * a.b_bytes : sa + a.a_bytes;
+            const uint32_t wb_lo = a.wres_bytes ? wb + a.n_kc * a.b_bytes : wb + off_lo;
+            const uint32_t tapb = (uint32_t)nch * a.BN * 16;   // bytes of one tap's weights in the box
+            // consecutive MMAs go to the mtv independent accumulators of the super tile
+            for (int tap = 0; tap < a.taps; ++tap) {
+              const uint32_t as = sa + base_pos * 16 + (uint32_t)a.tapoff[tap];
+              for (int kk = 0; kk < nch / 2; ++kk) {
+                const uint64_t bd = ptx::smem_desc(wb + tap * tapb + kk * 2 * (a.BN * 16), a.BN * 16, 128);
+                const uint32_t acc0 = (kcc > 0 || tap > 0 || kk > 0) ? 1u : 0u;
+                for (int j = 0; j < mtv; ++j) {
+                  const uint64_t ad = ptx::smem_desc(as + j * 2048 + kk * 2 * a.plane_bytes, a.plane_bytes, 128);
+                  ptx::umma(dtm + j * a.BN, ad, bd, idesc, acc0);
+                }
+#if PST_SPLIT
+                const uint64_t bdl = ptx::smem_desc(wb_lo + tap * tapb + kk * 2 * (a.BN * 16), a.BN * 16, 128);
+                for (int j = 0; j < mtv; ++j) {
+                  const uint64_t ad = ptx::smem_desc(as + j * 2048 + kk * 2 * a.plane_bytes, a.plane_bytes, 128);
+                  ptx::umma(dtm + j * a.BN, ad, bdl, idesc, 1u);
+                }
+                for (int j = 0; j < mtv; ++j) {
+                  const uint64_t adl =
+                      ptx::smem_desc(as + off_lo + j * 2048 + kk * 2 * a.plane_bytes, a.plane_bytes, 128);
+                  ptx::umma(dtm + j * a.BN, adl, bd, idesc, 1u);
+                }
+#endif
+              }
+            }
+            ptx::umma_commit(&empty[st]);
+            TL(4, dbg_i[4]++);
+            if (++st == a.stages) { st = 0; ph ^= 1; }
+          }
+          ptx::umma_commit(&tfull[acc]);
+          continue;
+        }
         int kiter = 0;
         for (int tap = 0; tap < a.taps; ++tap) {
           for (int kcc = 0; kcc < a.n_kc; ++kcc, ++kiter) {
             ptx::mbar_wait(PST_SPLIT ? &ready[st] : &full[st], ph);
+            TL(3, dbg_i[3]++);
             ptx::tc_fence_after();
             const uint32_t sa = ptx::smem_u32(ring + st * a.stage_bytes);
             const uint32_t sb = sa + a.a_bytes;
@@ -218,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t accum = (kiter > 0 || kk > 0) ? 1u : 0u;
               ptx::umma(dtm, ad, bd, idesc, accum);
 #if PST_SPLIT
-              const uint32_t off_lo = a.a_bytes + a.b_bytes;
+              const uint32_t off_lo = a.a_bytes + a.sb_bytes;
               const uint64_t adl = ptx::smem_desc(sa + off_lo + kk * 2 * 2048, 2048, 128);
               const uint64_t bdl = ptx::smem_desc(sb + off_lo + kk * 2 * (a.BN * 16), a.BN * 16, 128);
               ptx::umma(dtm, ad, bdl, idesc, 1u);
@@ -226,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
             }
             ptx::umma_commit(&empty[st]);
+            TL(4, dbg_i[4]++);
             if (++st == a.stages) { st = 0; ph ^= 1; }
           }
         }
@@ -243,17 +355,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = local & 1;
       const uint32_t use = (uint32_t)(local >> 1);
       ptx::mbar_wait(&tfull[acc], use & 1);
+      if (threadIdx.x == 64) TL(5, dbg_i[5]++);
       ptx::tc_fence_after();
+      const int g0s = HALO ? (mt % a.tpi) * 128 * a.MT : 0;
+      const int mts = HALO ? min(a.MT, (a.Pimg - g0s + 127) / 128) : 1;
+      for (int j = 0; j < mts; ++j) {
       int n, y, x;
-      decode_tile_px(a, mt, row, n, y, x);
+      if (HALO) {
+        n = mt / a.tpi;
+        const int g = g0s + j * 128 + row;
+        y = g / a.Wv;
+        x = g % a.Wv;
+      } else {
+        decode_tile_px(a, mt, row, n, y, x);
+      }
       const bool valid = (n < a.N) && (y < a.Ho) && (x < a.Wo);
       const int64_t pix = ((int64_t)n * a.Ho + y) * a.Wo + x;
       const int64_t npix = (int64_t)a.N * a.Ho * a.Wo;
       for (int ch = 0; ch < a.BN / 16; ++ch) {
         float v[16];
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * a.BN + ch * 16;
+        const uint32_t col = HALO ? (uint32_t)((acc * a.MT + j) * a.BN) : (uint32_t)(acc * a.BN);
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + col + ch * 16;
         ptx::tmem_ld16(taddr, v);
-        if (ch == a.BN / 16 - 1) {
+        if (ch == a.BN / 16 - 1 && j == mts - 1) {
           ptx::tc_fence_before();
           if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
         }
@@ -313,6 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::named_bar_sync(1, kEpiThreads);
         }
       }
+      }  // sub-tiles j
+      if (threadIdx.x == 64) TL(6, dbg_i[6]++);
     }
     if (a.epi == EPI_BN_STATS) {
       ptx::named_bar_sync(1, kEpiThreads);
@@ -326,13 +452,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int st = 0;
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
-      for (int kit = 0; kit < a.taps * a.n_kc; ++kit) {
+      for (int kit = 0; kit < (HALO ? 1 : a.taps) * a.n_kc; ++kit) {
         ptx::mbar_wait(&full[st], ph);
+        if (ct == 0) TL(1, dbg_i[1]++);
         uint8_t* sa = ring + st * a.stage_bytes;
-        split_lo(sa, sa + a.a_bytes + a.b_bytes, a.a_bytes, ct);
+        split_lo(sa, sa + a.a_bytes + a.sb_bytes, a.a_bytes, ct);
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&ready[st]);
+        if (ct == 0) TL(2, dbg_i[2]++);
         if (++st == a.stages) { st = 0; ph ^= 1; }
       }
     }
@@ -576,11 +704,14 @@ struct WbArgs {
   uint32_t rawx_bytes, rawx_tx, rawd_bytes, a_bytes, d_bytes, stage_bytes, sbo;
   uint32_t tmem_cols;
   float* part;
+  unsigned long long* dbg;
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
     conv_wgrad_band_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD,
                            const WbArgs a) {
+  int dbg_i[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (threadIdx.x == 0) TL(7, 0);
   extern __shared__ __align__(1024) uint8_t smem[];
   // stage: [raw X][raw dY][A hi][A lo][D hi][D lo]
   uint8_t* ring = smem;
@@ -633,6 +764,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = u_lo; u < u_hi; ++u) {
         const int n0 = (u / a.ny) * a.nb, y0 = (u % a.ny) * a.bh;
         ptx::mbar_wait(&empty[st], ph ^ 1);
+        TL(0, dbg_i[0]++);
         ptx::mbar_expect_tx(&full[st], a.rawx_tx + a.rawd_bytes);
         uint8_t* s0 = ring + st * a.stage_bytes;
         ptx::tma_load_4d(s0, &tmX, &full[st], -a.pad * kEPC, y0 * a.S - a.pad, n0, pl0);
@@ -648,22 +780,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       for (int it = 0; it < n_iter; ++it) {
         ptx::mbar_wait(&ready[st], ph);
+        TL(3, dbg_i[3]++);
         ptx::tc_fence_after();
         const uint32_t s0 = ptx::smem_u32(ring + st * a.stage_bytes);
         const uint32_t ahi = s0 + off_a, alo = ahi + a.a_bytes, dhi = s0 + off_d, dlo = dhi + a.d_bytes;
-        for (int j = 0; j < g_cnt; ++j) {
-          const uint32_t dt = tmem_base + j * a.BNw;
-          for (int kk = 0; kk < a.P8 / 8; ++kk) {
+        // consecutive MMAs target different accumulators (M tiles) so the tensor pipe
+        // is not serialised on one accumulator's read-modify-write latency
+        for (int kk = 0; kk < a.P8 / 8; ++kk) {
+          const uint64_t bd = ptx::smem_desc(dhi + kk * 256, 128, a.sbo);
+          const uint64_t bdl = ptx::smem_desc(dlo + kk * 256, 128, a.sbo);
+          for (int j = 0; j < g_cnt; ++j) {
             const uint64_t ad = ptx::smem_desc(ahi + j * mtile + kk * 256, 128, a.sbo);
+            ptx::umma(tmem_base + j * a.BNw, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+          }
+          for (int j = 0; j < g_cnt; ++j) {
+            const uint64_t ad = ptx::smem_desc(ahi + j * mtile + kk * 256, 128, a.sbo);
+            ptx::umma(tmem_base + j * a.BNw, ad, bdl, idesc, 1u);
+          }
+          for (int j = 0; j < g_cnt; ++j) {
             const uint64_t adl = ptx::smem_desc(alo + j * mtile + kk * 256, 128, a.sbo);
-            const uint64_t bd = ptx::smem_desc(dhi + kk * 256, 128, a.sbo);
-            const uint64_t bdl = ptx::smem_desc(dlo + kk * 256, 128, a.sbo);
-            ptx::umma(dt, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
-            ptx::umma(dt, ad, bdl, idesc, 1u);
-            ptx::umma(dt, adl, bd, idesc, 1u);
+            ptx::umma(tmem_base + j * a.BNw, adl, bd, idesc, 1u);
           }
         }
         ptx::umma_commit(&empty[st]);
+        TL(4, dbg_i[4]++);
         if (++st == a.stages) { st = 0; ph ^= 1; }
       }
       ptx::umma_commit(&tfull[0]);
@@ -675,6 +815,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(&tfull[0], 0);
       ptx::tc_fence_after();
     }
+    if (threadIdx.x == 64) TL(5, 0);
     for (int j = 0; j < g_cnt; ++j) {
       const int rg = r0 + j * 128 + rowl;
       for (int ch = 0; ch < a.BNw / 16; ++ch) {
@@ -697,12 +838,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ct = threadIdx.x - kBaseThreads;
     const int hw = a.bh * a.Wo;
     const int nq = a.P8 / 4;
-    const int unitsA = (g_cnt * 128 / 4) * nq;
-    const int unitsD = (a.BNw / 4) * nq;
+    const int unitsA = (g_cnt * 128) * nq;   // tasks: operand rows x pixel quads
+    const int unitsD = a.BNw * nq;
+    // gather tables (float index into the raw band): row part (plane, tap shift, lane) and
+    // pixel part (image, row, column); -1 marks padding rows / pixels
+    int* rowbase = reinterpret_cast<int*>(smem + a.stages * a.stage_bytes + (3 * kMaxStages + 2) * 8 + 16);
+    int* pixb = rowbase + g_cnt * 128;
+    for (int m = ct; m < g_cnt * 128; m += 128) {
+      const int R = r0 + m;
+      if (R >= r_end) { rowbase[m] = -1; continue; }
+      const int tap = R / a.Cinp, ci = R % a.Cinp;
+      const int r = tap / a.k, s = tap % a.k;
+      const int plane = ci / kEPC - pl0;
+      rowbase[m] = ((plane * a.nb * a.band_r + r) * a.band_c + s) * 4 + ci % kEPC;
+    }
+    for (int p = ct; p < a.P8; p += 128) {
+      if (p >= a.P) { pixb[p] = -1; continue; }
+      const int jj = p / hw, py = (p / a.Wo) % a.bh, px = p % a.Wo;
+      pixb[p] = ((jj * a.band_r + py * a.S) * a.band_c + px * a.S) * 4;
+    }
+    ptx::named_bar_sync(2, 128);
     int st = 0;
     uint32_t ph = 0;
     for (int it = 0; it < n_iter; ++it) {
       ptx::mbar_wait(&full[st], ph);
+      if (ct == 0) TL(1, dbg_i[1]++);
       uint8_t* s0 = ring + st * a.stage_bytes;
       const uint8_t* rawx = s0;
       const uint8_t* rawd = s0 + off_rawd;
@@ -710,48 +870,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint8_t* alo = ahi + a.a_bytes;
       uint8_t* dhi = s0 + off_d;
       uint8_t* dlo = dhi + a.d_bytes;
-      for (int u = ct; u < unitsA + unitsD; u += 128) {
-        const bool isA = u < unitsA;
-        const int uu = isA ? u : u - unitsA;
-        const int q4 = uu / nq, pq = uu % nq;
-        float4 v[4];
+      // one task = one operand row x 4 pixels (a K-major 16-byte row segment); a warp's
+      // 32 tasks = 8 rows x 4 pixel-quads = one contiguous 512-byte run (conflict-free stores)
+      const float* rawxf = reinterpret_cast<const float*>(rawx);
+      const float* rawdf = reinterpret_cast<const float*>(rawd);
+      const int arows = g_cnt * 128;
+      for (int u = ct; u < (unitsA + unitsD); u += 128) {
+        const int rr = u & 7, kq = (u >> 3) % nq, rg8 = (u >> 3) / nq;
+        const int m = rg8 * 8 + rr;
+        const bool isA = m < arows;
+        float hv[4];
         if (isA) {
-          const int R = r0 + 4 * q4;
-          const int tap = R / a.Cinp, ci = R % a.Cinp;
-          const int r = tap / a.k, s = tap % a.k;
-          const int plane = ci / kEPC - pl0;
+          const int rb = rowbase[m];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int p = 4 * pq + i;
-            v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (R < r_end && p < a.P) {
-              const int jj = p / hw, py = (p / a.Wo) % a.bh, px = p % a.Wo;
-              const int off = ((plane * a.nb + jj) * a.band_r + py * a.S + r) * a.band_c + px * a.S + s;
-              v[i] = *reinterpret_cast<const float4*>(rawx + off * 16);
-            }
+            const int pb = pixb[4 * kq + i];
+            hv[i] = (rb >= 0 && pb >= 0) ? rawxf[rb + pb] : 0.f;
           }
         } else {
+          const int co = m - arows;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int p = 4 * pq + i;
-            v[i] = p < a.P ? *reinterpret_cast<const float4*>(rawd + (q4 * a.P + p) * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const int p = 4 * kq + i;
+            hv[i] = p < a.P ? rawdf[((co >> 2) * a.P + p) * 4 + (co & 3)] : 0.f;
           }
         }
+        const int ml = isA ? m : m - arows;
+        const uint32_t off = (uint32_t)((ml >> 3) * a.sbo + kq * 128 + (ml & 7) * 16);
         uint8_t* hi = isA ? ahi : dhi;
         uint8_t* lo = isA ? alo : dlo;
-        const float* f = reinterpret_cast<const float*>(v);   // f[px*4 + ch]
-#pragma unroll
-        for (int cl = 0; cl < 4; ++cl) {
-          const int rr = 4 * q4 + cl;
-          const uint32_t off = (uint32_t)((rr >> 3) * a.sbo + pq * 128 + (rr & 7) * 16);
-          const float4 h = make_float4(f[cl], f[4 + cl], f[8 + cl], f[12 + cl]);
-          *reinterpret_cast<float4*>(hi + off) = h;
-          *reinterpret_cast<float4*>(lo + off) = make_float4(tf32_lo(h.x), tf32_lo(h.y), tf32_lo(h.z), tf32_lo(h.w));
-        }
+        *reinterpret_cast<float4*>(hi + off) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+        *reinterpret_cast<float4*>(lo + off) =
+            make_float4(tf32_lo(hv[0]), tf32_lo(hv[1]), tf32_lo(hv[2]), tf32_lo(hv[3]));
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&ready[st]);
+      if (ct == 0) TL(2, dbg_i[2]++);
       if (++st == a.stages) { st = 0; ph ^= 1; }
     }
   }
@@ -809,16 +964,16 @@ inline bool act_tmap_is4d(int S, int bw) { return S == 1 && bw * kEPC <= 256; }
 //  BN*EPC <= 256: dims (Coutp*EPC, Cinp/EPC, taps), box (BN*EPC, nch, 1) -- long rows;
 //  else         : dims (EPC, Coutp, Cinp/EPC, taps), box (EPC, BN, nch, 1).
 inline bool w_tmap_is3d(int BN) { return BN * kEPC <= 256; }
-CUtensorMap w_tmap(const act_t* p, int taps, int Coutp, int Cinp, int BN, int nch) {
+CUtensorMap w_tmap(const act_t* p, int taps, int Coutp, int Cinp, int BN, int nch, int box_taps = 1) {
   if (w_tmap_is3d(BN)) {
     uint64_t wd[3] = {(uint64_t)Coutp * kEPC, (uint64_t)Cinp / kEPC, (uint64_t)taps};
     uint64_t ws[2] = {(uint64_t)Coutp * 16, (uint64_t)Coutp * Cinp * sizeof(act_t)};
-    uint32_t wb[3] = {(uint32_t)(BN * kEPC), (uint32_t)nch, 1};
+    uint32_t wb[3] = {(uint32_t)(BN * kEPC), (uint32_t)nch, (uint32_t)box_taps};
     return make_tmap(act_tmap_dtype(), 3, p, wd, ws, wb, nullptr);
   }
   uint64_t wd[4] = {(uint64_t)kEPC, (uint64_t)Coutp, (uint64_t)Cinp / kEPC, (uint64_t)taps};
   uint64_t ws[3] = {16, (uint64_t)Coutp * 16, (uint64_t)Coutp * Cinp * sizeof(act_t)};
-  uint32_t wb[4] = {(uint32_t)kEPC, (uint32_t)BN, (uint32_t)nch, 1};
+  uint32_t wb[4] = {(uint32_t)kEPC, (uint32_t)BN, (uint32_t)nch, (uint32_t)box_taps};
   return make_tmap(act_tmap_dtype(), 4, p, wd, ws, wb, nullptr);
 }
 
@@ -855,27 +1010,93 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
   a.k = c.k; a.taps = c.k * c.k; a.S = c.S; a.off = c.off; a.sgn = c.sgn;
   a.Coutp = c.Coutp; a.Cout = c.Cout;
   const int nch = a.kc / kEPC;
-  a.a_bytes = (uint32_t)nch * 2048;
-  a.b_bytes = (uint32_t)nch * a.BN * 16;
-  a.tx_bytes = a.a_bytes + a.b_bytes * (PST_SPLIT ? 2 : 1);
-  a.stage_bytes = (a.a_bytes + a.b_bytes) * (PST_SPLIT ? 2 : 1);
   const int budget = 190 * 1024;
-  a.stages = std::max(2, std::min(kMaxStages, budget / (int)a.stage_bytes));
-  a.tmem_cols = (uint32_t)std::max(32, pow2_at_least(2 * a.BN));
+  const int xsplit = PST_SPLIT ? 2 : 1;
+  // ---- HALO plan (stride 1, wide images): virtual grid of pitch Wv, one band per tile
+  bool halo = false;
+  int nch_h = nch;
+  static const bool halo_on = std::getenv("PST_HALO") != nullptr;   // experimental (slower today)
+  if (halo_on && c.S == 1 && c.k > 1 && c.Wo >= 16 && 128 % c.Wo == 0 && (c.Ho * c.Wo) % 128 == 0) {
+    const int o1 = c.off, o2 = c.off + c.sgn * (c.k - 1);
+    const int lo = std::min(o1, o2), hi = std::max(o1, o2);
+    const int Wv = c.Wo;   // band copies are exactly one output row wide
+    // candidates: M tiles per super tile (independent accumulators) x channels per stage
+    for (int MT : {1, 2}) {
+      if (halo) break;
+      if (2 * MT * a.BN > 512) continue;
+      for (int kc = a.kc; kc >= 2 * kEPC && !halo; kc -= 2 * kEPC) {
+        if (c.Cinp % kc) continue;
+        const int nc = kc / kEPC, nkc = c.Cinp / kc;
+        const int band_r = (MT * 128) / Wv + (hi - lo);
+        const uint32_t plane = (uint32_t)band_r * Wv * 16;
+        if (Wv * kEPC > 256 || band_r > 256 || plane >= (1u << 18)) continue;
+        const uint32_t ab = plane * nc * c.k;   // k column-shifted copies
+        const uint32_t bb = (uint32_t)a.taps * nc * a.BN * 16;      // one chunk, all taps
+        const uint32_t wres_all = bb * nkc * xsplit;
+        const bool wres = (a.n_ntiles == 1) && wres_all <= 96 * 1024;
+        const uint32_t sb = wres ? 0 : bb;
+        const uint32_t stage = (ab + sb) * xsplit;
+        const int stages = std::min(kMaxStages, (int)((budget - (wres ? wres_all : 0)) / stage));
+        if (stages < 2) continue;
+        halo = true;
+        nch_h = nc;
+        a.kc = kc; a.n_kc = nkc;
+        a.Wv = Wv; a.lo = lo; a.MT = MT;
+        a.Pimg = c.Ho * Wv;
+        a.tpi = ceil_div(a.Pimg, 128 * MT);
+        a.n_mtiles = c.N * a.tpi;
+        a.n_tiles = a.n_mtiles * a.n_ntiles;
+        a.plane_bytes = plane;
+        a.a_bytes = ab; a.b_bytes = bb; a.sb_bytes = sb;
+        a.wres_bytes = wres ? wres_all : 0;
+        a.tx_bytes = ab + sb * xsplit;
+        a.stage_bytes = stage;
+        a.stages = stages;
+        for (int t = 0; t < a.taps; ++t) {
+          const int oy = c.off + c.sgn * (t / c.k), ox = c.off + c.sgn * (t % c.k);
+          a.tapoff[t] = (ox - lo) * nc * (int)plane + (oy - lo) * Wv * 16;   // bytes
+        }
+      }
+    }
+  }
+  if (!halo) {
+    a.a_bytes = (uint32_t)nch * 2048;
+    a.b_bytes = (uint32_t)nch * a.BN * 16;
+    a.sb_bytes = a.b_bytes;
+    a.wres_bytes = 0;
+    a.tx_bytes = a.a_bytes + a.b_bytes * xsplit;
+    a.stage_bytes = (a.a_bytes + a.b_bytes) * xsplit;
+    a.stages = std::max(2, std::min(kMaxStages, budget / (int)a.stage_bytes));
+  }
+  a.tmem_cols = (uint32_t)std::max(32, pow2_at_least(2 * a.BN * (halo ? a.MT : 1)));
   a.epi = c.epi; a.relu = c.relu; a.out = c.out; a.bias = c.bias; a.stats = c.stats;
   a.res = c.res; a.res_mode = c.res_mode; a.res_H = c.res_H; a.res_W = c.res_W; a.res_C = c.res_C;
   a.res_pad = c.res_pad;
+  a.dbg = c.dbg;
 
-  a.a4 = act_tmap_is4d(c.S, a.bw) ? 1 : 0;
+  a.a4 = halo ? 1 : (act_tmap_is4d(c.S, a.bw) ? 1 : 0);
   a.b3 = w_tmap_is3d(a.BN) ? 1 : 0;
-  CUtensorMap tA = act_tmap(c.in, c.N, c.H, c.W, c.Cinp, a.bimg, a.bh, a.bw, c.S, nch);
-  CUtensorMap tB = w_tmap(c.wshadow, a.taps, c.Coutp, c.Cinp, a.BN, nch);
-  CUtensorMap tBlo =
-      PST_SPLIT ? w_tmap(c.wshadow + (size_t)a.taps * c.Coutp * c.Cinp, a.taps, c.Coutp, c.Cinp, a.BN, nch) : tB;
-  const size_t smem = (size_t)a.stages * a.stage_bytes + (16 * 129 + 4) * 4 + 2 * c.Coutp * 8 +
-                      (3 * kMaxStages + 4) * 8 + 16;
+  CUtensorMap tA;
+  if (halo) {  // band box: (Wv*EPC, band_r, 1 image, nch planes)
+    const int band_r = (int)(a.plane_bytes / (a.Wv * 16));
+    uint64_t dims[4] = {(uint64_t)c.W * kEPC, (uint64_t)c.H, (uint64_t)c.N, (uint64_t)c.Cinp / kEPC};
+    uint64_t str[3] = {(uint64_t)c.W * 16, (uint64_t)c.H * c.W * 16, (uint64_t)c.N * c.H * c.W * 16};
+    uint32_t box[4] = {(uint32_t)(a.Wv * kEPC), (uint32_t)band_r, 1, (uint32_t)nch_h};
+    tA = make_tmap(act_tmap_dtype(), 4, c.in, dims, str, box, nullptr);
+  } else {
+    tA = act_tmap(c.in, c.N, c.H, c.W, c.Cinp, a.bimg, a.bh, a.bw, c.S, nch);
+  }
+  const int btaps = halo ? a.taps : 1;
+  const int nch_b = halo ? nch_h : nch;
+  CUtensorMap tB = w_tmap(c.wshadow, a.taps, c.Coutp, c.Cinp, a.BN, nch_b, btaps);
+  CUtensorMap tBlo = PST_SPLIT ? w_tmap(c.wshadow + (size_t)a.taps * c.Coutp * c.Cinp, a.taps, c.Coutp, c.Cinp, a.BN,
+                                        nch_b, btaps)
+                               : tB;
+  const size_t smem = (size_t)a.stages * a.stage_bytes + a.wres_bytes + (16 * 129 + 4) * 4 + 2 * c.Coutp * 8 +
+                      (3 * kMaxStages + 5) * 8 + 16;
   PST_CHECK_ARG(smem <= 227 * 1024, "conv smem budget");
-  PST_CUDA(cudaFuncSetAttribute(conv_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (halo) PST_CUDA(cudaFuncSetAttribute(conv_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  else PST_CUDA(cudaFuncSetAttribute(conv_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev;
   PST_CUDA(cudaGetDevice(&dev));
   const int grid = std::min(a.n_tiles, num_sms(dev));
@@ -886,7 +1107,8 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
                        (c.res ? (double)c.N * c.res_H * c.res_W * c.res_C * es : 0.0);
   const double flops = 2.0 * c.N * c.Ho * c.Wo * c.Coutp * (double)c.Cinp * a.taps;
   prof::begin(st);
-  conv_fwd_kernel<<<grid, kThreads, smem, st>>>(tA, tB, tBlo, a);
+  if (halo) conv_fwd_kernel<true><<<grid, kThreads, smem, st>>>(tA, tB, tBlo, a);
+  else conv_fwd_kernel<false><<<grid, kThreads, smem, st>>>(tA, tB, tBlo, a);
   PST_CUDA(cudaGetLastError());
   prof::end(st, c.epi == EPI_DGRAD ? prof::CONV_DGRAD : prof::CONV_FWD, bytes, flops);
 }
@@ -980,6 +1202,7 @@ void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
   if (b.G >= 1) {
     PST_CHECK_ARG(b.ksplit == w.ksplit, "wgrad: workspace planned for a different split");
     b.part = w.part;
+    b.dbg = w.dbg;
     // X: dims (W*EPC, H, N, Cinp/EPC), box (band_c*EPC, band_r, nb, pl_grp)
     uint64_t xd[4] = {(uint64_t)w.W * kEPC, (uint64_t)w.H, (uint64_t)w.N, (uint64_t)w.Cinp / kEPC};
     uint64_t xs[3] = {(uint64_t)w.W * 16, (uint64_t)w.H * w.W * 16, (uint64_t)w.N * w.H * w.W * 16};
@@ -990,7 +1213,7 @@ void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
     uint64_t ds[3] = {(uint64_t)w.Wo * 16, (uint64_t)w.Ho * w.Wo * 16, (uint64_t)w.N * w.Ho * w.Wo * 16};
     uint32_t db[4] = {(uint32_t)(w.Wo * kEPC), (uint32_t)b.bh, (uint32_t)b.nb, (uint32_t)(b.BNw / kEPC)};
     CUtensorMap tD = make_tmap(act_tmap_dtype(), 4, w.dy, dd, ds, db, nullptr);
-    const size_t smem = (size_t)b.stages * b.stage_bytes + (3 * kMaxStages + 2) * 8 + 16;
+    const size_t smem = (size_t)b.stages * b.stage_bytes + (3 * kMaxStages + 2) * 8 + 16 + (size_t)(b.G * 128 + b.P8) * 4;
     PST_CHECK_ARG(smem <= 227 * 1024, "wgrad smem budget");
     PST_CUDA(cudaFuncSetAttribute(conv_wgrad_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = b.n_mgroups * b.n_ntiles * b.ksplit;

@@ -34,6 +34,7 @@ struct ConvSpec {
   const act_t* res;         // EPI_DGRAD residual gradient (identity or option A) or null
   int res_mode;             // 0 none, 1 identity, 2 option A
   int res_H, res_W, res_C, res_pad;
+  unsigned long long* dbg;  // optional device timeline buffer [8][256] (CTA 0), debug only
 };
 void conv_tc(const ConvSpec& c, cudaStream_t st);
 
@@ -45,6 +46,7 @@ struct WgradSpec {
   int k, S, pad;
   float* part;              // workspace, ksplit * rows * Coutp floats
   int ksplit;               // chosen by wgrad_plan
+  unsigned long long* dbg;  // optional device timeline buffer [8][256] (CTA 0), debug only
 };
 struct WgradPlan { int ksplit; int64_t part_floats; };
 WgradPlan wgrad_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm);

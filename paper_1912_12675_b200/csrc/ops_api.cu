@@ -1,4 +1,6 @@
 // ops_api.cu -- include/pst_ops.h: single convolution passes on the tcgen05 path.
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -67,7 +69,20 @@ int pst_op_conv2d_fwd(const float* x, const float* w, float* y, int N, int Cin, 
     c.Ho = g.Ho; c.Wo = g.Wo; c.Coutp = g.Coutp; c.Cout = Cout;
     c.k = k; c.S = stride; c.off = -pad; c.sgn = 1;
     c.wshadow = sf; c.epi = EPI_BIAS_F32; c.out = yo;
+    const bool tl = std::getenv("PST_DBG_TL") != nullptr;
+    if (tl) c.dbg = s.get<unsigned long long>(8 * 256);
     conv_tc(c, 0);
+    if (tl) {  // debug: print CTA 0's timeline (us since kernel start)
+      std::vector<unsigned long long> h(8 * 256);
+      PST_CUDA(cudaMemcpy(h.data(), c.dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+      const char* names[8] = {"prod_issue", "conv_full", "conv_ready", "mma_start", "mma_commit", "epi_start",
+                              "epi_done", "start"};
+      for (int e = 0; e < 7; ++e) {
+        std::printf("TL %-10s", names[e]);
+        for (int i = 0; i < 24 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (h[e * 256 + i] - h[7 * 256]) / 1e3);
+        std::printf("\n");
+      }
+    }
     act_to_nchw(yo, 1, y, N, Cout, g.Ho, g.Wo, 0);
     PST_CUDA(cudaDeviceSynchronize());
   });
@@ -120,7 +135,20 @@ int pst_op_conv2d_wgrad(const float* x, const float* gy, float* gw, int N, int C
     wg.x = xa; wg.N = N; wg.H = H; wg.W = W; wg.Cinp = g.Cinp;
     wg.dy = ga; wg.Ho = g.Ho; wg.Wo = g.Wo; wg.Coutp = g.Coutp;
     wg.k = k; wg.S = stride; wg.pad = pad; wg.part = part; wg.ksplit = p.ksplit;
+    const bool tl = std::getenv("PST_DBG_TL") != nullptr;
+    if (tl) wg.dbg = s.get<unsigned long long>(8 * 256);
     conv_wgrad_tc(wg, 0);
+    if (tl) {
+      std::vector<unsigned long long> h(8 * 256);
+      PST_CUDA(cudaMemcpy(h.data(), wg.dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+      const char* names[8] = {"prod_issue", "conv_full", "conv_ready", "mma_start", "mma_commit", "epi_start",
+                              "epi_done", "start"};
+      for (int e = 0; e < 6; ++e) {
+        std::printf("TLW %-10s", names[e]);
+        for (int i = 0; i < 24 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (h[e * 256 + i] - h[7 * 256]) / 1e3);
+        std::printf("\n");
+      }
+    }
     wgrad_reduce(part, p.ksplit, g.Coutp, g.Cinp, Cout, Cin, k, gw, 0);
     PST_CUDA(cudaDeviceSynchronize());
   });
