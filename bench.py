@@ -254,12 +254,34 @@ def main():
         except Exception:
             traffic = None
     step_ms_prof = sum(v[0] for v in prof.values()) / max(1, args.profile_steps)
-    roofline = {"bound": "hbm", "kernel": cls, "achieved": achieved, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
-                "frac": achieved / pk.get("hbm_gbs", 6555.8), "traffic": traffic,
-                "alg_bytes_per_launch": kbytes / max(1, kn), "launches": kn, "avg_launch_us": 1e3 * kms / max(1, kn),
+    # Roofline of the dominant kernel class: the binding resource is the one whose lower-bound
+    # time (algorithmic bytes / HBM peak vs algorithmic flops / tensor peak) is larger.
+    # Tensor peak for the default build's fp32 contraction: 3 TF32 products per fp32 product
+    # (3xTF32), TF32 = measured bf16 peak x the guide's nominal 1.1/2.25 ratio.
+    info = pst.build_info()
+    hbm_peak = pk.get("hbm_gbs", 6650.0)
+    bf16_peak = pk.get("bf16_tflops", 1590.0)
+    if "tf32x3" in info:
+        tc_peak, tc_note = bf16_peak * (1.1 / 2.25) / 3.0, "bf16_tflops x 1.1/2.25 (tf32) / 3 (3xTF32 products)"
+    else:
+        tc_peak, tc_note = bf16_peak, "bf16_tflops"
+    t_bw = kbytes / (hbm_peak * 1e9) if kbytes else 0.0
+    t_tc = kflops / (tc_peak * 1e12) if kflops else 0.0
+    tflops = kflops / (kms / 1e3) / 1e12 if kms > 0 else 0.0
+    if t_tc > t_bw:
+        bound, ach, peak, unit = "tensor", tflops, tc_peak, "TFLOP/s"
+        src = "MEASURED_PEAKS.json " + tc_note + ("" if not pk.get("fallback") else " of fallback")
+    else:
+        bound, ach, peak, unit = "hbm", achieved, hbm_peak, "GB/s"
+        src = "MEASURED_PEAKS.json hbm_gbs (burst copy)" + ("" if not pk.get("fallback") else " of fallback")
+    roofline = {"bound": bound, "kernel": cls, "achieved": ach, "peak": peak, "unit": unit,
+                "frac": ach / peak if peak else None, "traffic": traffic,
+                "alg_bytes_per_launch": kbytes / max(1, kn), "alg_flops_per_launch": kflops / max(1, kn),
+                "launches": kn, "avg_launch_us": 1e3 * kms / max(1, kn),
                 "share_of_step": (kms / max(1, args.profile_steps)) / step_ms_prof if step_ms_prof else None,
-                "tensor_tflops": kflops / (kms / 1e3) / 1e12 if kms > 0 else 0.0,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+                "hbm_gbs": achieved, "tensor_tflops": tflops,
+                "frac_of_roofline_time": (max(t_bw, t_tc) / (kms / 1e3)) if kms > 0 else None,
+                "peak_source": src}
     kernel_table = {k: {"ms_per_step": v[0] / max(1, args.profile_steps), "launches_per_step": v[1] / max(1, args.profile_steps),
                         "GBps": (v[2] / (v[0] / 1e3) / 1e9) if v[0] > 0 else 0.0,
                         "TFLOPs": (v[3] / (v[0] / 1e3) / 1e12) if v[0] > 0 else 0.0}

@@ -147,7 +147,8 @@ __device__ __forceinline__ unsigned long long gtime() {
 // positions read for EVERY tap; tap (oy, ox) is then just the band shifted by
 // (oy-lo)*Wv + (ox-lo) positions -- a descriptor start offset, no re-load.  Weights of
 // all taps stay resident in smem when they fit.
-template <bool HALO>
+// DG distinguishes the dgrad instantiation (same code, separate name in profiles).
+template <bool HALO, bool DG>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmBlo, const FwdArgs a) {
@@ -1095,8 +1096,10 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
   const size_t smem = (size_t)a.stages * a.stage_bytes + a.wres_bytes + (16 * 129 + 4) * 4 + 2 * c.Coutp * 8 +
                       (3 * kMaxStages + 5) * 8 + 16;
   PST_CHECK_ARG(smem <= 227 * 1024, "conv smem budget");
-  if (halo) PST_CUDA(cudaFuncSetAttribute(conv_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  else PST_CUDA(cudaFuncSetAttribute(conv_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const bool dg = c.epi == EPI_DGRAD;
+  auto kern = halo ? (dg ? conv_fwd_kernel<true, true> : conv_fwd_kernel<true, false>)
+                   : (dg ? conv_fwd_kernel<false, true> : conv_fwd_kernel<false, false>);
+  PST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev;
   PST_CUDA(cudaGetDevice(&dev));
   const int grid = std::min(a.n_tiles, num_sms(dev));
@@ -1107,8 +1110,7 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
                        (c.res ? (double)c.N * c.res_H * c.res_W * c.res_C * es : 0.0);
   const double flops = 2.0 * c.N * c.Ho * c.Wo * c.Coutp * (double)c.Cinp * a.taps;
   prof::begin(st);
-  if (halo) conv_fwd_kernel<true><<<grid, kThreads, smem, st>>>(tA, tB, tBlo, a);
-  else conv_fwd_kernel<false><<<grid, kThreads, smem, st>>>(tA, tB, tBlo, a);
+  kern<<<grid, kThreads, smem, st>>>(tA, tB, tBlo, a);
   PST_CUDA(cudaGetLastError());
   prof::end(st, c.epi == EPI_DGRAD ? prof::CONV_DGRAD : prof::CONV_FWD, bytes, flops);
 }
@@ -1219,7 +1221,7 @@ void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
     const int grid = b.n_mgroups * b.n_ntiles * b.ksplit;
     const double es = sizeof(act_t);
     const double bytes = (double)w.N * w.H * w.W * w.Cinp * es + (double)w.N * w.Ho * w.Wo * w.Coutp * es +
-                         (double)b.ksplit * b.rows * w.Coutp * 4.0;
+                         (double)b.rows * w.Coutp * 4.0;   // algorithmic: X + dY read, dW written once
     const double flops = 2.0 * b.rows * (double)w.Coutp * w.N * w.Ho * w.Wo;
     prof::begin(st);
     conv_wgrad_band_kernel<<<grid, kThreads, smem, st>>>(tX, tD, b);
@@ -1259,7 +1261,7 @@ void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
   const int grid = a.n_mgroups * a.n_ntiles * a.ksplit;
   const double es = sizeof(act_t);
   const double bytes = (double)w.N * w.H * w.W * w.Cinp * es + (double)w.N * w.Ho * w.Wo * w.Coutp * es +
-                       (double)a.ksplit * a.rows * w.Coutp * 4.0;
+                       (double)a.rows * w.Coutp * 4.0;   // algorithmic: X + dY read, dW written once
   const double flops = 2.0 * a.rows * (double)w.Coutp * w.N * w.Ho * w.Wo;
   prof::begin(st);
   conv_wgrad_kernel<<<grid, kThreads, smem, st>>>(tX, tD, a);
