@@ -222,8 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             TL(0, dbg_i[0]++);
             ptx::mbar_expect_tx(&full[st], a.tx_bytes);
             uint8_t* sa = ring + st * a.stage_bytes;
-            for (int cx = 0; cx < a.k; ++cx)   // k column-shifted copies: every tap start is 128-B aligned
-              tma_act(sa + cx * nch * a.plane_bytes, &tmA, &full[st], true, a.lo + cx, yf + a.lo, n, kcc * nch);
+            // one band box: rows [yf+lo, yf+lo+band_r) x columns [lo, lo+Wv), zero outside the image
+            tma_act(sa, &tmA, &full[st], true, a.lo, yf + a.lo, n, kcc * nch);
             if (!a.wres_bytes) {
               uint8_t* sb = sa + a.a_bytes;
               tma_w(sb, &tmB, &full[st], a.b3, nt * a.BN, kcc * nch, 0);
@@ -258,92 +258,91 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = ptx::idesc_mma(128, a.BN, 0, 0, PST_AB_FORMAT);
-      int st = 0;
-      uint32_t ph = 0;
-      int local = 0;
-      if (HALO && a.wres_bytes) ptx::mbar_wait(wbar, 0);
-      for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++local) {
-        const int acc = local & 1;
-        const uint32_t use = (uint32_t)(local >> 1);
-        ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t dtm = tmem_base + acc * a.BN * (HALO ? a.MT : 1);
-        if (HALO) {
-          const int mt = t / a.n_ntiles;
-          const int g0 = (mt % a.tpi) * 128 * a.MT;
-          const int mtv = min(a.MT, (a.Pimg - g0 + 127) / 128);         // M tiles with valid rows
-          const uint32_t base_pos = (uint32_t)(g0 - (g0 / a.Wv) * a.Wv);   // g0 relative to its band row
-          for (int kcc = 0; kcc < a.n_kc; ++kcc) {
-            ptx::mbar_wait(PST_SPLIT ? &ready[st] : &full[st], ph);
-            TL(3, dbg_i[3]++);
-            ptx::tc_fence_after();
-            const uint32_t sa = ptx::smem_u32(ring + st * a.stage_bytes);
-            const uint32_t off_lo = a.a_bytes + a.sb_bytes;
-            const uint32_t wb = a.wres_bytes ? ptx::smem_u32(wres) + kcc * a.b_bytes : sa + a.a_bytes;
-            const uint32_t wb_lo = a.wres_bytes ? wb + a.n_kc * a.b_bytes : wb + off_lo;
-            const uint32_t tapb = (uint32_t)nch * a.BN * 16;   // bytes of one tap's weights in the box
+    // ------------------------------------------------------------ MMA issuer (warp-uniform, elected lane)
+    const uint32_t idesc = ptx::idesc_mma(128, a.BN, 0, 0, PST_AB_FORMAT);
+    int st = 0;
+    uint32_t ph = 0;
+    int local = 0;
+    if (HALO && a.wres_bytes) ptx::mbar_wait(wbar, 0);
+    for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t use = (uint32_t)(local >> 1);
+      ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t dtm = tmem_base + acc * a.BN * (HALO ? a.MT : 1);
+      if (HALO) {
+        const int mt = t / a.n_ntiles;
+        const int g0 = (mt % a.tpi) * 128 * a.MT;
+        const int mtv = min(a.MT, (a.Pimg - g0 + 127) / 128);         // M tiles with valid rows
+        const uint32_t base_pos = (uint32_t)(g0 - (g0 / a.Wv) * a.Wv);   // g0 relative to its band row
+        for (int kcc = 0; kcc < a.n_kc; ++kcc) {
+          ptx::mbar_wait(PST_SPLIT ? &ready[st] : &full[st], ph);
+          if (lane == 0) TL(3, dbg_i[3]++);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(ring + st * a.stage_bytes);
+          const uint32_t off_lo = a.a_bytes + a.sb_bytes;
+          const uint32_t wb = a.wres_bytes ? ptx::smem_u32(wres) + kcc * a.b_bytes : sa + a.a_bytes;
+          const uint32_t wb_lo = a.wres_bytes ? wb + a.n_kc * a.b_bytes : wb + off_lo;
+          const uint32_t tapb = (uint32_t)nch * a.BN * 16;   // bytes of one tap's weights in the box
+          const uint64_t bd0 = ptx::smem_desc(wb, a.BN * 16, 128);
+          const uint64_t bdl0 = ptx::smem_desc(wb_lo, a.BN * 16, 128);
+          const uint64_t ad0 = ptx::smem_desc(sa + base_pos * 16, a.plane_bytes, 128);
+          if (ptx::elect_one()) {
             // consecutive MMAs go to the mtv independent accumulators of the super tile
             for (int tap = 0; tap < a.taps; ++tap) {
-              const uint32_t as = sa + base_pos * 16 + (uint32_t)a.tapoff[tap];
+              const uint64_t adt = ptx::desc_add(ad0, (uint32_t)a.tapoff[tap]);
               for (int kk = 0; kk < nch / 2; ++kk) {
-                const uint64_t bd = ptx::smem_desc(wb + tap * tapb + kk * 2 * (a.BN * 16), a.BN * 16, 128);
+                const uint64_t bd = ptx::desc_add(bd0, tap * tapb + kk * 2 * (a.BN * 16));
+                const uint64_t adk = ptx::desc_add(adt, kk * 2 * a.plane_bytes);
                 const uint32_t acc0 = (kcc > 0 || tap > 0 || kk > 0) ? 1u : 0u;
-                for (int j = 0; j < mtv; ++j) {
-                  const uint64_t ad = ptx::smem_desc(as + j * 2048 + kk * 2 * a.plane_bytes, a.plane_bytes, 128);
-                  ptx::umma(dtm + j * a.BN, ad, bd, idesc, acc0);
-                }
+                for (int j = 0; j < mtv; ++j) ptx::umma(dtm + j * a.BN, ptx::desc_add(adk, j * 2048), bd, idesc, acc0);
 #if PST_SPLIT
-                const uint64_t bdl = ptx::smem_desc(wb_lo + tap * tapb + kk * 2 * (a.BN * 16), a.BN * 16, 128);
-                for (int j = 0; j < mtv; ++j) {
-                  const uint64_t ad = ptx::smem_desc(as + j * 2048 + kk * 2 * a.plane_bytes, a.plane_bytes, 128);
-                  ptx::umma(dtm + j * a.BN, ad, bdl, idesc, 1u);
-                }
-                for (int j = 0; j < mtv; ++j) {
-                  const uint64_t adl =
-                      ptx::smem_desc(as + off_lo + j * 2048 + kk * 2 * a.plane_bytes, a.plane_bytes, 128);
-                  ptx::umma(dtm + j * a.BN, adl, bd, idesc, 1u);
-                }
+                const uint64_t bdl = ptx::desc_add(bdl0, tap * tapb + kk * 2 * (a.BN * 16));
+                for (int j = 0; j < mtv; ++j) ptx::umma(dtm + j * a.BN, ptx::desc_add(adk, j * 2048), bdl, idesc, 1u);
+                for (int j = 0; j < mtv; ++j)
+                  ptx::umma(dtm + j * a.BN, ptx::desc_add(adk, off_lo + j * 2048), bd, idesc, 1u);
 #endif
               }
             }
             ptx::umma_commit(&empty[st]);
-            TL(4, dbg_i[4]++);
-            if (++st == a.stages) { st = 0; ph ^= 1; }
           }
-          ptx::umma_commit(&tfull[acc]);
-          continue;
+          __syncwarp();
+          if (lane == 0) TL(4, dbg_i[4]++);
+          if (++st == a.stages) { st = 0; ph ^= 1; }
         }
-        int kiter = 0;
-        for (int tap = 0; tap < a.taps; ++tap) {
-          for (int kcc = 0; kcc < a.n_kc; ++kcc, ++kiter) {
-            ptx::mbar_wait(PST_SPLIT ? &ready[st] : &full[st], ph);
-            TL(3, dbg_i[3]++);
-            ptx::tc_fence_after();
-            const uint32_t sa = ptx::smem_u32(ring + st * a.stage_bytes);
-            const uint32_t sb = sa + a.a_bytes;
+        if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);
+        __syncwarp();
+        continue;
+      }
+      const uint32_t off_lo = a.a_bytes + a.sb_bytes;
+      int kiter = 0;
+      for (int tap = 0; tap < a.taps; ++tap) {
+        for (int kcc = 0; kcc < a.n_kc; ++kcc, ++kiter) {
+          ptx::mbar_wait(PST_SPLIT ? &ready[st] : &full[st], ph);
+          if (lane == 0) TL(3, dbg_i[3]++);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(ring + st * a.stage_bytes);
+          const uint64_t ad0 = ptx::smem_desc(sa, 2048, 128);
+          const uint64_t bd0 = ptx::smem_desc(sa + a.a_bytes, a.BN * 16, 128);
+          if (ptx::elect_one()) {
             for (int kk = 0; kk < nch / 2; ++kk) {
-              const uint64_t ad = ptx::smem_desc(sa + kk * 2 * 2048, 2048, 128);
-              const uint64_t bd = ptx::smem_desc(sb + kk * 2 * (a.BN * 16), a.BN * 16, 128);
-              const uint32_t accum = (kiter > 0 || kk > 0) ? 1u : 0u;
-              ptx::umma(dtm, ad, bd, idesc, accum);
+              const uint64_t ad = ptx::desc_add(ad0, kk * 2 * 2048);
+              const uint64_t bd = ptx::desc_add(bd0, kk * 2 * (a.BN * 16));
+              ptx::umma(dtm, ad, bd, idesc, (kiter > 0 || kk > 0) ? 1u : 0u);
 #if PST_SPLIT
-              const uint32_t off_lo = a.a_bytes + a.sb_bytes;
-              const uint64_t adl = ptx::smem_desc(sa + off_lo + kk * 2 * 2048, 2048, 128);
-              const uint64_t bdl = ptx::smem_desc(sb + off_lo + kk * 2 * (a.BN * 16), a.BN * 16, 128);
-              ptx::umma(dtm, ad, bdl, idesc, 1u);
-              ptx::umma(dtm, adl, bd, idesc, 1u);
+              ptx::umma(dtm, ad, ptx::desc_add(bd, off_lo), idesc, 1u);
+              ptx::umma(dtm, ptx::desc_add(ad, off_lo), bd, idesc, 1u);
 #endif
             }
             ptx::umma_commit(&empty[st]);
-            TL(4, dbg_i[4]++);
-            if (++st == a.stages) { st = 0; ph ^= 1; }
           }
+          __syncwarp();
+          if (lane == 0) TL(4, dbg_i[4]++);
+          if (++st == a.stages) { st = 0; ph ^= 1; }
         }
-        ptx::umma_commit(&tfull[acc]);
       }
+      if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);
+      __syncwarp();
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------ epilogue (warps 2..5)
@@ -745,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < a.stages; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
-      ptx::mbar_init(&ready[i], 4);
+      ptx::mbar_init(&ready[i], 8);
     }
     ptx::mbar_init(&tfull[0], 1);
     ptx::fence_mbar_init();
@@ -774,141 +773,155 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && n_iter > 0) {
+    if (n_iter > 0) {
       const uint32_t idesc = ptx::idesc_mma(128, a.BNw, 0, 0, PST_AB_FORMAT);
       const uint32_t mtile = 16 * a.sbo;   // 128 rows
       int st = 0;
       uint32_t ph = 0;
       for (int it = 0; it < n_iter; ++it) {
         ptx::mbar_wait(&ready[st], ph);
-        TL(3, dbg_i[3]++);
+        if (lane == 0) TL(3, dbg_i[3]++);
         ptx::tc_fence_after();
         const uint32_t s0 = ptx::smem_u32(ring + st * a.stage_bytes);
-        const uint32_t ahi = s0 + off_a, alo = ahi + a.a_bytes, dhi = s0 + off_d, dlo = dhi + a.d_bytes;
-        // consecutive MMAs target different accumulators (M tiles) so the tensor pipe
-        // is not serialised on one accumulator's read-modify-write latency
-        for (int kk = 0; kk < a.P8 / 8; ++kk) {
-          const uint64_t bd = ptx::smem_desc(dhi + kk * 256, 128, a.sbo);
-          const uint64_t bdl = ptx::smem_desc(dlo + kk * 256, 128, a.sbo);
-          for (int j = 0; j < g_cnt; ++j) {
-            const uint64_t ad = ptx::smem_desc(ahi + j * mtile + kk * 256, 128, a.sbo);
-            ptx::umma(tmem_base + j * a.BNw, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+        const uint64_t ad0 = ptx::smem_desc(s0 + off_a, 128, a.sbo);
+        const uint64_t bd0 = ptx::smem_desc(s0 + off_d, 128, a.sbo);
+        if (ptx::elect_one()) {
+          // consecutive MMAs target different accumulators (M tiles)
+          for (int kk = 0; kk < a.P8 / 8; ++kk) {
+            const uint64_t bd = ptx::desc_add(bd0, kk * 256);
+            const uint64_t bdl = ptx::desc_add(bd, a.d_bytes);
+            const uint64_t ak = ptx::desc_add(ad0, kk * 256);
+            for (int j = 0; j < g_cnt; ++j)
+              ptx::umma(tmem_base + j * a.BNw, ptx::desc_add(ak, j * mtile), bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+            for (int j = 0; j < g_cnt; ++j)
+              ptx::umma(tmem_base + j * a.BNw, ptx::desc_add(ak, j * mtile), bdl, idesc, 1u);
+            for (int j = 0; j < g_cnt; ++j)
+              ptx::umma(tmem_base + j * a.BNw, ptx::desc_add(ak, a.a_bytes + j * mtile), bd, idesc, 1u);
           }
-          for (int j = 0; j < g_cnt; ++j) {
-            const uint64_t ad = ptx::smem_desc(ahi + j * mtile + kk * 256, 128, a.sbo);
-            ptx::umma(tmem_base + j * a.BNw, ad, bdl, idesc, 1u);
-          }
-          for (int j = 0; j < g_cnt; ++j) {
-            const uint64_t adl = ptx::smem_desc(alo + j * mtile + kk * 256, 128, a.sbo);
-            ptx::umma(tmem_base + j * a.BNw, adl, bd, idesc, 1u);
-          }
+          ptx::umma_commit(&empty[st]);
         }
-        ptx::umma_commit(&empty[st]);
-        TL(4, dbg_i[4]++);
+        __syncwarp();
+        if (lane == 0) TL(4, dbg_i[4]++);
         if (++st == a.stages) { st = 0; ph ^= 1; }
       }
-      ptx::umma_commit(&tfull[0]);
-    }
-  } else if (warp < 6) {
-    const int q = warp & 3;
-    const int rowl = q * 32 + lane;
-    if (n_iter > 0) {
-      ptx::mbar_wait(&tfull[0], 0);
-      ptx::tc_fence_after();
-    }
-    if (threadIdx.x == 64) TL(5, 0);
-    for (int j = 0; j < g_cnt; ++j) {
-      const int rg = r0 + j * 128 + rowl;
-      for (int ch = 0; ch < a.BNw / 16; ++ch) {
-        float v[16];
-        if (n_iter > 0) {
-          ptx::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + j * a.BNw + ch * 16, v);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-        }
-        if (rg < a.rows) {
-          float4* op = reinterpret_cast<float4*>(a.part + ((int64_t)ks * a.rows + rg) * a.Coutp + nt * a.BNw + ch * 16);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        }
-      }
+      if (ptx::elect_one()) ptx::umma_commit(&tfull[0]);
+      __syncwarp();
     }
   } else {
-    // converter: raw band / raw dY -> K-major hi/lo operands (4 rows x 4 pixels per unit)
-    const int ct = threadIdx.x - kBaseThreads;
+    // Warps 2..9 convert every stage (raw band / raw dY -> K-major hi/lo operands); warps
+    // 2..5 then drain the accumulators.  One task = 4 operand rows (one 16-byte channel
+    // quad of one tap) x 4 pixels: four 16-byte loads (one per pixel) transposed into four
+    // 16-byte K-major row segments.  Lane bits: 0 = row-quad parity, 1-2 = pixel quad (low),
+    // which also rotates the store order -> the 8 lanes of each 16-byte store phase hit 8
+    // distinct bank quads.
+    const int ct = threadIdx.x - 64;            // 0..255
     const int hw = a.bh * a.Wo;
     const int nq = a.P8 / 4;
-    const int unitsA = (g_cnt * 128) * nq;   // tasks: operand rows x pixel quads
-    const int unitsD = a.BNw * nq;
-    // gather tables (float index into the raw band): row part (plane, tap shift, lane) and
-    // pixel part (image, row, column); -1 marks padding rows / pixels
+    const int nqh = (nq + 3) / 4;
+    const int arows = g_cnt * 128;
+    const int mqA = arows / 4, mqD = a.BNw / 4;
     int* rowbase = reinterpret_cast<int*>(smem + a.stages * a.stage_bytes + (3 * kMaxStages + 2) * 8 + 16);
     int* pixb = rowbase + g_cnt * 128;
-    for (int m = ct; m < g_cnt * 128; m += 128) {
-      const int R = r0 + m;
-      if (R >= r_end) { rowbase[m] = -1; continue; }
+    for (int mq = ct; mq < mqA; mq += 256) {
+      const int R = r0 + 4 * mq;
+      if (R >= r_end) { rowbase[mq] = -1; continue; }
       const int tap = R / a.Cinp, ci = R % a.Cinp;
-      const int r = tap / a.k, s = tap % a.k;
+      const int r = tap / a.k, s2 = tap % a.k;
       const int plane = ci / kEPC - pl0;
-      rowbase[m] = ((plane * a.nb * a.band_r + r) * a.band_c + s) * 4 + ci % kEPC;
+      rowbase[mq] = ((plane * a.nb * a.band_r + r) * a.band_c + s2) * 4;
     }
-    for (int p = ct; p < a.P8; p += 128) {
+    for (int p = ct; p < a.P8; p += 256) {
       if (p >= a.P) { pixb[p] = -1; continue; }
       const int jj = p / hw, py = (p / a.Wo) % a.bh, px = p % a.Wo;
       pixb[p] = ((jj * a.band_r + py * a.S) * a.band_c + px * a.S) * 4;
     }
-    ptx::named_bar_sync(2, 128);
+    ptx::named_bar_sync(2, 256);
+    const int par = ct & 1, kql = (ct >> 1) & 3;
+    const int rot = kql;                        // store / load rotation
+    const int tasksA = (mqA / 2) * nqh, tasksD = ((mqD + 1) / 2) * nqh;
     int st = 0;
     uint32_t ph = 0;
     for (int it = 0; it < n_iter; ++it) {
       ptx::mbar_wait(&full[st], ph);
       if (ct == 0) TL(1, dbg_i[1]++);
       uint8_t* s0 = ring + st * a.stage_bytes;
-      const uint8_t* rawx = s0;
-      const uint8_t* rawd = s0 + off_rawd;
+      const float* rawxf = reinterpret_cast<const float*>(s0);
+      const float* rawdf = reinterpret_cast<const float*>(s0 + off_rawd);
       uint8_t* ahi = s0 + off_a;
       uint8_t* alo = ahi + a.a_bytes;
       uint8_t* dhi = s0 + off_d;
       uint8_t* dlo = dhi + a.d_bytes;
-      // one task = one operand row x 4 pixels (a K-major 16-byte row segment); a warp's
-      // 32 tasks = 8 rows x 4 pixel-quads = one contiguous 512-byte run (conflict-free stores)
-      const float* rawxf = reinterpret_cast<const float*>(rawx);
-      const float* rawdf = reinterpret_cast<const float*>(rawd);
-      const int arows = g_cnt * 128;
-      for (int u = ct; u < (unitsA + unitsD); u += 128) {
-        const int rr = u & 7, kq = (u >> 3) % nq, rg8 = (u >> 3) / nq;
-        const int m = rg8 * 8 + rr;
-        const bool isA = m < arows;
-        float hv[4];
+      for (int rest = ct >> 3; rest < tasksA + tasksD; rest += 32) {
+        const bool isA = rest < tasksA;
+        const int rr = isA ? rest : rest - tasksA;
+        const int kq = (rr % nqh) * 4 + kql;
+        const int mq = (rr / nqh) * 2 + par;
+        if (kq >= nq || (!isA && mq >= mqD)) continue;
+        float4 v[4];
         if (isA) {
-          const int rb = rowbase[m];
+          const int rb = rowbase[mq];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int pb = pixb[4 * kq + i];
-            hv[i] = (rb >= 0 && pb >= 0) ? rawxf[rb + pb] : 0.f;
+            v[i] = (rb >= 0 && pb >= 0) ? *reinterpret_cast<const float4*>(rawxf + rb + pb)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         } else {
-          const int co = m - arows;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int p = 4 * kq + i;
-            hv[i] = p < a.P ? rawdf[((co >> 2) * a.P + p) * 4 + (co & 3)] : 0.f;
+            v[i] = p < a.P ? *reinterpret_cast<const float4*>(rawdf + ((int64_t)mq * a.P + p) * 4)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
-        const int ml = isA ? m : m - arows;
-        const uint32_t off = (uint32_t)((ml >> 3) * a.sbo + kq * 128 + (ml & 7) * 16);
         uint8_t* hi = isA ? ahi : dhi;
         uint8_t* lo = isA ? alo : dlo;
-        *reinterpret_cast<float4*>(hi + off) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-        *reinterpret_cast<float4*>(lo + off) =
-            make_float4(tf32_lo(hv[0]), tf32_lo(hv[1]), tf32_lo(hv[2]), tf32_lo(hv[3]));
+        const uint32_t base = (uint32_t)((mq >> 1) * a.sbo + kq * 128 + (mq & 1) * 64);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = (j + rot) & 3;          // row c of the quad = channel c over the 4 pixels
+          float4 h;
+          if (c == 0) h = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+          else if (c == 1) h = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+          else if (c == 2) h = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
+          else h = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+          const uint32_t off = base + c * 16;
+          *reinterpret_cast<float4*>(hi + off) = h;
+          *reinterpret_cast<float4*>(lo + off) = make_float4(tf32_lo(h.x), tf32_lo(h.y), tf32_lo(h.z), tf32_lo(h.w));
+        }
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&ready[st]);
       if (ct == 0) TL(2, dbg_i[2]++);
       if (++st == a.stages) { st = 0; ph ^= 1; }
+    }
+    if (warp < 6) {
+      // epilogue: accumulators -> split-K partials
+      const int q = warp & 3;
+      const int rowl = q * 32 + lane;
+      if (n_iter > 0) {
+        ptx::mbar_wait(&tfull[0], 0);
+        ptx::tc_fence_after();
+      }
+      if (threadIdx.x == 64) TL(5, 0);
+      for (int j = 0; j < g_cnt; ++j) {
+        const int rg = r0 + j * 128 + rowl;
+        for (int ch = 0; ch < a.BNw / 16; ++ch) {
+          float v[16];
+          if (n_iter > 0) {
+            ptx::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + j * a.BNw + ch * 16, v);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          }
+          if (rg < a.rows) {
+            float4* op = reinterpret_cast<float4*>(a.part + ((int64_t)ks * a.rows + rg) * a.Coutp + nt * a.BNw + ch * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+        }
+      }
     }
   }
   ptx::tc_fence_before();
@@ -993,6 +1006,7 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
   PST_CHECK_ARG(c.Cinp % 16 == 0 && c.Coutp % 16 == 0, "conv channels must be padded to 16");
   PST_CHECK_ARG(c.S == 1 || c.S == 2, "conv stride must be 1 or 2");
   PST_CHECK_ARG((reinterpret_cast<uintptr_t>(c.in) & 15) == 0, "conv input must be 16B aligned");
+  if (conv_ts(c, st)) return;   // activation operand in TMEM (conv_ts.cu) where the tiling fits
   FwdArgs a{};
   a.N = c.N; a.Ho = c.Ho; a.Wo = c.Wo;
   pixel_tile(c.N, c.Ho, c.Wo, 128, a.bimg, a.bh, a.bw);
@@ -1016,27 +1030,30 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
   // ---- HALO plan (stride 1, wide images): virtual grid of pitch Wv, one band per tile
   bool halo = false;
   int nch_h = nch;
-  static const bool halo_on = std::getenv("PST_HALO") != nullptr;   // experimental (slower today)
-  if (halo_on && c.S == 1 && c.k > 1 && c.Wo >= 16 && 128 % c.Wo == 0 && (c.Ho * c.Wo) % 128 == 0) {
-    const int o1 = c.off, o2 = c.off + c.sgn * (c.k - 1);
-    const int lo = std::min(o1, o2), hi = std::max(o1, o2);
-    const int Wv = c.Wo;   // band copies are exactly one output row wide
+  // HALO by default where it applies (PST_NOHALO=1: per-tap loads everywhere, for comparison)
+  static const bool halo_on = std::getenv("PST_NOHALO") == nullptr;
+  const int o1 = c.off, o2 = c.off + c.sgn * (c.k - 1);
+  const int lo = std::min(o1, o2), hi = std::max(o1, o2);
+  const int Wv = c.Wo + (hi - lo);   // virtual-grid row pitch = band row = output row + halo columns
+  if (halo_on && c.S == 1 && c.k > 1 && c.Wo >= 16 && Wv * kEPC <= 256) {
     // candidates: M tiles per super tile (independent accumulators) x channels per stage
-    for (int MT : {1, 2}) {
+    for (int MT : {2, 1}) {
       if (halo) break;
       if (2 * MT * a.BN > 512) continue;
       for (int kc = a.kc; kc >= 2 * kEPC && !halo; kc -= 2 * kEPC) {
         if (c.Cinp % kc) continue;
         const int nc = kc / kEPC, nkc = c.Cinp / kc;
-        const int band_r = (MT * 128) / Wv + (hi - lo);
+        // rows spanned by 128*MT consecutive positions starting anywhere in a row, + halo rows
+        const int band_r = (128 * MT + Wv - 2) / Wv + 1 + (hi - lo);
         const uint32_t plane = (uint32_t)band_r * Wv * 16;
-        if (Wv * kEPC > 256 || band_r > 256 || plane >= (1u << 18)) continue;
-        const uint32_t ab = plane * nc * c.k;   // k column-shifted copies
+        if (band_r > 256 || plane >= (1u << 18)) continue;
+        const uint32_t ab_tx = plane * nc;                           // band box bytes
+        const uint32_t ab = (uint32_t)round_up((int)ab_tx, 128);     // smem footprint (128-B aligned)
         const uint32_t bb = (uint32_t)a.taps * nc * a.BN * 16;      // one chunk, all taps
         const uint32_t wres_all = bb * nkc * xsplit;
         const bool wres = (a.n_ntiles == 1) && wres_all <= 96 * 1024;
         const uint32_t sb = wres ? 0 : bb;
-        const uint32_t stage = (ab + sb) * xsplit;
+        const uint32_t stage = round_up((int)((ab + sb) * xsplit), 128);
         const int stages = std::min(kMaxStages, (int)((budget - (wres ? wres_all : 0)) / stage));
         if (stages < 2) continue;
         halo = true;
@@ -1050,12 +1067,12 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
         a.plane_bytes = plane;
         a.a_bytes = ab; a.b_bytes = bb; a.sb_bytes = sb;
         a.wres_bytes = wres ? wres_all : 0;
-        a.tx_bytes = ab + sb * xsplit;
+        a.tx_bytes = ab_tx + sb * xsplit;
         a.stage_bytes = stage;
         a.stages = stages;
         for (int t = 0; t < a.taps; ++t) {
           const int oy = c.off + c.sgn * (t / c.k), ox = c.off + c.sgn * (t % c.k);
-          a.tapoff[t] = (ox - lo) * nc * (int)plane + (oy - lo) * Wv * 16;   // bytes
+          a.tapoff[t] = ((oy - lo) * Wv + (ox - lo)) * 16;   // bytes: a 16-B aligned row shift
         }
       }
     }

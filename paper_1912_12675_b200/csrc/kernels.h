@@ -37,6 +37,9 @@ struct ConvSpec {
   unsigned long long* dbg;  // optional device timeline buffer [8][256] (CTA 0), debug only
 };
 void conv_tc(const ConvSpec& c, cudaStream_t st);
+// TS-mode variant (A operand in tensor memory, 3xTF32 build); returns false if the shape
+// does not fit its tiling (conv_tc then runs the smem-operand kernel).
+bool conv_ts(const ConvSpec& c, cudaStream_t st);
 
 // Weight gradient dW[tap*Cinp+ci][co] = sum_pixels X(shifted by tap)[p][ci] * dY[p][co],
 // split over pixel ranges: part[ks][rows][Coutp] float32 (reduced by sgd_update).

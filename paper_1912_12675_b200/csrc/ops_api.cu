@@ -75,11 +75,10 @@ int pst_op_conv2d_fwd(const float* x, const float* w, float* y, int N, int Cin, 
     if (tl) {  // debug: print CTA 0's timeline (us since kernel start)
       std::vector<unsigned long long> h(8 * 256);
       PST_CUDA(cudaMemcpy(h.data(), c.dbg, h.size() * 8, cudaMemcpyDeviceToHost));
-      const char* names[8] = {"prod_issue", "conv_full", "conv_ready", "mma_start", "mma_commit", "epi_start",
-                              "epi_done", "start"};
+      const char* names[8] = {"prod_issue", "ev1", "ev2", "ev3", "ev4", "epi_start", "epi_done", "start"};
       for (int e = 0; e < 7; ++e) {
         std::printf("TL %-10s", names[e]);
-        for (int i = 0; i < 24 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (h[e * 256 + i] - h[7 * 256]) / 1e3);
+        for (int i = 0; i < 40 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (h[e * 256 + i] - h[7 * 256]) / 1e3);
         std::printf("\n");
       }
     }
@@ -145,7 +144,7 @@ int pst_op_conv2d_wgrad(const float* x, const float* gy, float* gw, int N, int C
                               "epi_done", "start"};
       for (int e = 0; e < 6; ++e) {
         std::printf("TLW %-10s", names[e]);
-        for (int i = 0; i < 24 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (h[e * 256 + i] - h[7 * 256]) / 1e3);
+        for (int i = 0; i < 40 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (h[e * 256 + i] - h[7 * 256]) / 1e3);
         std::printf("\n");
       }
     }

@@ -1,0 +1,3 @@
+timeout 600 python -m pytest tests/test_gpu_ops.py -x -q > gpurun_out/t6.log 2>&1; echo rc=$? >> gpurun_out/t6.log
+timeout 600 python -m pytest tests/test_gpu_pipeline.py -x -q >> gpurun_out/t6.log 2>&1; echo rc=$? >> gpurun_out/t6.log
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/b6.json 2> gpurun_out/b6.err
