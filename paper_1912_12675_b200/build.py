@@ -18,7 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["common.cpp", "model.cpp", "conv_tc.cu", "conv_ts.cu", "elementwise.cu", "stage.cu", "pst_api.cu", "ops_api.cu"]
+SOURCES = ["common.cpp", "model.cpp", "conv_tc.cu", "conv_ts.cu", "conv_wgrad_ts.cu", "elementwise.cu", "stage.cu", "pst_api.cu", "ops_api.cu"]
 
 
 def _deps_mtime():

@@ -1183,6 +1183,12 @@ WbArgs plan_band(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k
 
 WgradPlan wgrad_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm) {
 #if PST_SPLIT
+  if (const int ks = wgrad_ts_ksplit(N, H, W, Cinp, Ho, Wo, Coutp, k, S, pad, num_sm)) {
+    WgradPlan p;
+    p.ksplit = ks;
+    p.part_floats = (int64_t)ks * k * k * Cinp * Coutp;
+    return p;
+  }
   {
     const WbArgs b = plan_band(N, H, W, Cinp, Ho, Wo, Coutp, k, S, pad, num_sm);
     if (b.G >= 1) {
@@ -1214,6 +1220,7 @@ WgradPlan wgrad_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, i
 
 void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
   PST_CHECK_ARG(w.Cinp % 16 == 0 && w.Coutp % 16 == 0, "wgrad channels must be padded to 16");
+  if (conv_wgrad_ts(w, st)) return;   // expanded input operand in TMEM (conv_wgrad_ts.cu)
 #if PST_SPLIT
   int dev_b;
   PST_CUDA(cudaGetDevice(&dev_b));

@@ -1,0 +1,356 @@
+// conv_wgrad_ts.cu -- weight gradient dW = X_shifted^T dY on tcgen05 with the expanded input
+// operand in TENSOR MEMORY (3xTF32 build).
+//
+//   dW[tap*Cinp + ci][co] = sum_p X[p shifted by tap][ci] * dY[p][co]
+//   M = rows (tap, ci), N = co, K = output pixels p.
+//
+// A (M x K) is the im2col expansion of the input.  The smem-operand design materialised it
+// (hi and lo planes, M padded to 128) in shared memory and re-read it three times per K step;
+// here each converter thread owns one row (= one TMEM lane) and writes that row's K values
+// straight into a TMEM slot with tcgen05.st (hi and lo), so the expansion costs one 4-byte
+// shared load per element and the MMAs read A from TMEM ("TS" form, tools/mma_bench.cu).
+//   warp 0     TMA: per stage one input band box (all taps' rows/cols of the stage's pixels)
+//              and one dY box
+//   warps 2-9  converters (two per TMEM lane quarter): A rows -> TMEM slot; dY -> K-major
+//              hi/lo B rows in smem
+//   warp 1     MMA: D_j += A_hi B_hi + A_hi B_lo + A_lo B_hi for the CTA's M tiles j
+//   warps 2-5  finally drain D into split-K partials part[ks][rows][Coutp]
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.h"
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace pst {
+
+#if PST_SPLIT
+namespace {
+
+constexpr int kWtThreads = 320;
+constexpr int kWtMaxSB = 8;
+constexpr int kWtMaxSlots = 8;
+
+struct WtArgs {
+  int N, H, W, Cinp, Ho, Wo, Coutp;
+  int k, S, pad;
+  int nb, bh, P, P16, band_r, band_c, ny, n_units;
+  int rows, n_mt, G, n_mgroups, BNw, n_ntiles, ksplit;
+  int pl_grp, pl_all;
+  int SB, St;                          // smem stages, TMEM A slots
+  uint32_t rawx_bytes, rawx_tx, rawd_bytes, b_bytes, stage_bytes, sboB;
+  float* part;
+};
+
+__global__ void __launch_bounds__(kWtThreads, 1)
+    conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD,
+                         const WtArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // [SB stages: raw X | raw dY | B hi | B lo] [pixel table P16 ints] [barriers] [tmem ptr]
+  uint8_t* ring = smem;
+  int* pixb = reinterpret_cast<int*>(smem + a.SB * a.stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pixb + 128);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kWtMaxSB;
+  uint64_t* ready = empty + kWtMaxSB;
+  uint64_t* afree = ready + kWtMaxSlots;
+  uint64_t* tfull = afree + kWtMaxSlots;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int b = blockIdx.x;
+  const int mg = b % a.n_mgroups;
+  const int nt = (b / a.n_mgroups) % a.n_ntiles;
+  const int ks = b / (a.n_mgroups * a.n_ntiles);
+  const int u_lo = (int)((int64_t)ks * a.n_units / a.ksplit);
+  const int u_hi = (int)((int64_t)(ks + 1) * a.n_units / a.ksplit);
+  const int n_iter = u_hi - u_lo;
+  const int mt0 = mg * a.G;
+  const int g_cnt = min(a.G, a.n_mt - mt0);
+  const int r0 = mt0 * 128;
+  const int r_end = min(r0 + g_cnt * 128, a.rows);
+  const int pl0 = a.pl_all ? 0 : (r0 % a.Cinp) / kEPC;
+  const uint32_t off_rawd = a.rawx_bytes;
+  const uint32_t off_b = off_rawd + ((a.rawd_bytes + 127u) & ~127u);
+  const uint32_t acc_cols = (uint32_t)a.G * a.BNw;       // accumulators: [0, G*BNw)
+  const uint32_t slot_cols = (uint32_t)a.G * 2 * a.P16;  // per slot: G tiles x (P16 hi + P16 lo)
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.SB; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < a.St; ++i) { ptx::mbar_init(&ready[i], 8); ptx::mbar_init(&afree[i], 1); }
+    ptx::mbar_init(tfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (threadIdx.x < a.P16) {   // pixel table: float offset of pixel p in the band (-1: padding)
+    const int p = threadIdx.x;
+    const int hw = a.bh * a.Wo;
+    if (p >= a.P) pixb[p] = -1;
+    else {
+      const int jj = p / hw, py = (p / a.Wo) % a.bh, px = p % a.Wo;
+      pixb[p] = ((jj * a.band_r + py * a.S) * a.band_c + px * a.S) * 4;
+    }
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_ptr, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (ptx::elect_one()) {
+      ptx::prefetch_tmap(&tmX);
+      ptx::prefetch_tmap(&tmD);
+    }
+    __syncwarp();
+    for (int it = 0; it < n_iter; ++it) {
+      const int sb = it % a.SB;
+      const int u = u_lo + it;
+      const int n0 = (u / a.ny) * a.nb, y0 = (u % a.ny) * a.bh;
+      ptx::mbar_wait(&empty[sb], ((it / a.SB) & 1) ^ 1);
+      if (ptx::elect_one()) {
+        uint8_t* s0 = ring + sb * a.stage_bytes;
+        ptx::mbar_expect_tx(&full[sb], a.rawx_tx + a.rawd_bytes);
+        ptx::tma_load_4d(s0, &tmX, &full[sb], -a.pad * kEPC, y0 * a.S - a.pad, n0, pl0);
+        ptx::tma_load_4d(s0 + off_rawd, &tmD, &full[sb], 0, y0, n0, nt * (a.BNw / kEPC));
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    const uint32_t idesc = ptx::idesc_mma(128, a.BNw, 0, 0, 2);
+    for (int it = 0; it < n_iter; ++it) {
+      const int sb = it % a.SB, slot = it % a.St;
+      ptx::mbar_wait(&ready[slot], (it / a.St) & 1);
+      ptx::tc_fence_after();
+      const uint64_t bd0 = ptx::smem_desc(ptx::smem_u32(ring + sb * a.stage_bytes + off_b), 128, a.sboB);
+      if (ptx::elect_one()) {
+        const uint32_t abase = tmem + acc_cols + slot * slot_cols;
+        for (int kk = 0; kk < a.P16 / 8; ++kk) {
+          const uint64_t bd = ptx::desc_add(bd0, kk * 256);
+          const uint64_t bdl = ptx::desc_add(bd, a.b_bytes);
+          const uint32_t acc0 = (it > 0 || kk > 0) ? 1u : 0u;
+          for (int j = 0; j < g_cnt; ++j) {
+            const uint32_t ahi = abase + j * 2 * a.P16 + kk * 8;
+            const uint32_t d = tmem + j * a.BNw;
+            ptx::umma_tf32_ts(d, ahi, bd, idesc, acc0);
+            ptx::umma_tf32_ts(d, ahi, bdl, idesc, 1u);
+            ptx::umma_tf32_ts(d, ahi + a.P16, bd, idesc, 1u);
+          }
+        }
+        ptx::umma_commit(&empty[sb]);
+        ptx::umma_commit(&afree[slot]);
+      }
+      __syncwarp();
+    }
+    if (n_iter > 0 && ptx::elect_one()) ptx::umma_commit(tfull);
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- converters (warps 2..9)
+    const int q = warp & 3;
+    const int set = (warp - 2) >> 2;            // 0 or 1: M tiles j = set, set+2, ...
+    const int ct = threadIdx.x - 64;            // 0..255
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    // this thread's A rows (one per owned M tile): float offset of (tap, ci) in the band
+    int rb[4] = {-1, -1, -1, -1};
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = set + 2 * jj;
+      const int R = r0 + j * 128 + q * 32 + lane;
+      if (j < g_cnt && R < r_end) {
+        const int tap = R / a.Cinp, ci = R % a.Cinp;
+        const int rr = tap / a.k, ss = tap % a.k;
+        const int plane = ci / kEPC - pl0;
+        rb[jj] = ((plane * a.nb * a.band_r + rr) * a.band_c + ss) * 4 + ci % kEPC;
+      }
+    }
+    const int nq = a.P16 / 4;
+    const int unitsB = (a.BNw / 4) * nq;
+    for (int it = 0; it < n_iter; ++it) {
+      const int sb = it % a.SB, slot = it % a.St;
+      ptx::mbar_wait(&full[sb], (it / a.SB) & 1);
+      ptx::mbar_wait(&afree[slot], ((it / a.St) & 1) ^ 1);
+      ptx::tc_fence_after();
+      uint8_t* s0 = ring + sb * a.stage_bytes;
+      const float* rawxf = reinterpret_cast<const float*>(s0);
+      const float* rawdf = reinterpret_cast<const float*>(s0 + off_rawd);
+      uint8_t* bhi = s0 + off_b;
+      uint8_t* blo = bhi + a.b_bytes;
+      // B: dY [co/4][P][4] -> K-major hi/lo rows (co) x pixels, 4 co x 4 px per task
+      for (int u = ct; u < unitsB; u += 256) {
+        const int kq = u % nq, cq = u / nq;
+        float4 v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int p = 4 * kq + i;
+          v[i] = p < a.P ? *reinterpret_cast<const float4*>(rawdf + ((int64_t)cq * a.P + p) * 4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int co = 4 * cq + c;
+          float4 h;
+          if (c == 0) h = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+          else if (c == 1) h = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+          else if (c == 2) h = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
+          else h = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+          const uint32_t off = (uint32_t)((co >> 3) * a.sboB + kq * 128 + (co & 7) * 16);
+          *reinterpret_cast<float4*>(bhi + off) = h;
+          *reinterpret_cast<float4*>(blo + off) = make_float4(tf32_lo(h.x), tf32_lo(h.y), tf32_lo(h.z), tf32_lo(h.w));
+        }
+      }
+      // A: this thread's rows -> TMEM slot (hi columns [0,P16), lo columns [P16, 2 P16) per tile)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = set + 2 * jj;
+        if (j >= g_cnt) break;
+        const uint32_t ta = tmem + lane_addr + acc_cols + slot * slot_cols + j * 2 * a.P16;
+        for (int p0 = 0; p0 < a.P16; p0 += 16) {
+          float hv[16], lv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int pb = pixb[p0 + i];
+            hv[i] = (rb[jj] >= 0 && pb >= 0) ? rawxf[rb[jj] + pb] : 0.f;
+            lv[i] = tf32_lo(hv[i]);
+          }
+          ptx::tmem_st16(ta + p0, hv);
+          ptx::tmem_st16(ta + a.P16 + p0, lv);
+        }
+      }
+      ptx::tmem_st_wait();
+      ptx::fence_proxy_async_smem();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&ready[slot]);
+    }
+    if (warp < 6) {
+      // ---------------------------------------------------------------- epilogue (warps 2..5)
+      if (n_iter > 0) {
+        ptx::mbar_wait(tfull, 0);
+        ptx::tc_fence_after();
+      }
+      for (int j = 0; j < g_cnt; ++j) {
+        const int R = r0 + j * 128 + q * 32 + lane;
+        for (int ch = 0; ch < a.BNw / 16; ++ch) {
+          float v[16];
+          if (n_iter > 0) {
+            ptx::tmem_ld16(tmem + lane_addr + j * a.BNw + ch * 16, v);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          }
+          if (R < a.rows) {
+            float4* op = reinterpret_cast<float4*>(a.part + ((int64_t)ks * a.rows + R) * a.Coutp + nt * a.BNw + ch * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+int tile_n16(int C, int cap) {
+  int best = 16;
+  for (int b = 16; b <= cap && b <= C; b += 16)
+    if (C % b == 0) best = b;
+  return best;
+}
+
+}  // namespace
+
+bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm,
+                   void* out) {
+  if (std::getenv("PST_NOTS") != nullptr) return false;
+  WtArgs a{};
+  a.N = N; a.H = H; a.W = W; a.Cinp = Cinp; a.Ho = Ho; a.Wo = Wo; a.Coutp = Coutp;
+  a.k = k; a.S = S; a.pad = pad;
+  a.rows = k * k * Cinp;
+  a.n_mt = ceil_div(a.rows, 128);
+  a.BNw = tile_n16(Coutp, 128);
+  a.n_ntiles = Coutp / a.BNw;
+  const int ptarget = 32;
+  if (Ho * Wo >= ptarget) { a.nb = 1; a.bh = std::max(1, std::min(Ho, ptarget / Wo)); }
+  else { a.nb = std::max(1, std::min(N, ptarget / (Ho * Wo))); a.bh = Ho; }
+  a.P = a.nb * a.bh * Wo;
+  a.P16 = round_up(a.P, 16);
+  if (a.P16 > 128) return false;
+  a.band_r = (a.bh - 1) * S + k;
+  a.band_c = (Wo - 1) * S + k;
+  if (a.band_c * kEPC > 256 || a.band_r > 256) return false;
+  // M tiles per CTA: largest G with >= 2 TMEM slots
+  a.G = 0;
+  for (int G = std::min(a.n_mt, 4); G >= 1; --G) {
+    const int slots = (512 - G * a.BNw) / (G * 2 * a.P16);
+    if (slots >= 2) { a.G = G; a.St = std::min(kWtMaxSlots, slots); break; }
+  }
+  if (a.G == 0) return false;
+  const bool all = (a.G * 128 >= Cinp) || (Cinp % (a.G * 128) != 0);
+  a.pl_all = all ? 1 : 0;
+  a.pl_grp = all ? Cinp / kEPC : a.G * 128 / kEPC;
+  if (a.pl_grp > 256) return false;
+  a.rawx_tx = (uint32_t)a.pl_grp * a.nb * a.band_r * a.band_c * 16;
+  a.rawx_bytes = (uint32_t)round_up((int)a.rawx_tx, 128);
+  a.rawd_bytes = (uint32_t)(a.BNw / kEPC) * a.P * 16;
+  a.b_bytes = (uint32_t)a.BNw * a.P16 * 4;
+  a.sboB = (uint32_t)(a.P16 / 4) * 128;
+  a.stage_bytes = (uint32_t)round_up((int)(a.rawx_bytes + round_up((int)a.rawd_bytes, 128) + 2 * a.b_bytes), 1024);
+  const int budget = 200 * 1024;
+  a.SB = std::min(kWtMaxSB, budget / (int)a.stage_bytes);
+  if (a.SB < 2) return false;
+  a.n_mgroups = ceil_div(a.n_mt, a.G);
+  a.ny = ceil_div(Ho, a.bh);
+  a.n_units = ceil_div(N, a.nb) * a.ny;
+  const int base = a.n_mgroups * a.n_ntiles;
+  a.ksplit = std::max(1, std::min(std::max(1, a.n_units / 2), num_sm / base));
+  if (out) *reinterpret_cast<WtArgs*>(out) = a;
+  return true;
+}
+
+int wgrad_ts_ksplit(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm) {
+  WtArgs a;
+  if (!wgrad_ts_plan(N, H, W, Cinp, Ho, Wo, Coutp, k, S, pad, num_sm, &a)) return 0;
+  return a.ksplit;
+}
+
+bool conv_wgrad_ts(const WgradSpec& w, cudaStream_t st) {
+  int dev;
+  PST_CUDA(cudaGetDevice(&dev));
+  WtArgs a;
+  if (!wgrad_ts_plan(w.N, w.H, w.W, w.Cinp, w.Ho, w.Wo, w.Coutp, w.k, w.S, w.pad, num_sms(dev), &a)) return false;
+  PST_CHECK_ARG(a.ksplit == w.ksplit, "wgrad: workspace planned for a different split");
+  a.part = w.part;
+  uint64_t xd[4] = {(uint64_t)w.W * kEPC, (uint64_t)w.H, (uint64_t)w.N, (uint64_t)w.Cinp / kEPC};
+  uint64_t xs[3] = {(uint64_t)w.W * 16, (uint64_t)w.H * w.W * 16, (uint64_t)w.N * w.H * w.W * 16};
+  uint32_t xb[4] = {(uint32_t)(a.band_c * kEPC), (uint32_t)a.band_r, (uint32_t)a.nb, (uint32_t)a.pl_grp};
+  CUtensorMap tX = make_tmap(act_tmap_dtype(), 4, w.x, xd, xs, xb, nullptr);
+  uint64_t dd[4] = {(uint64_t)w.Wo * kEPC, (uint64_t)w.Ho, (uint64_t)w.N, (uint64_t)w.Coutp / kEPC};
+  uint64_t ds[3] = {(uint64_t)w.Wo * 16, (uint64_t)w.Ho * w.Wo * 16, (uint64_t)w.N * w.Ho * w.Wo * 16};
+  uint32_t db[4] = {(uint32_t)(w.Wo * kEPC), (uint32_t)a.bh, (uint32_t)a.nb, (uint32_t)(a.BNw / kEPC)};
+  CUtensorMap tD = make_tmap(act_tmap_dtype(), 4, w.dy, dd, ds, db, nullptr);
+  const size_t smem = (size_t)a.SB * a.stage_bytes + 128 * 4 + (2 * kWtMaxSB + 2 * kWtMaxSlots + 1) * 8 + 16;
+  PST_CHECK_ARG(smem <= 227 * 1024, "wgrad smem budget");
+  PST_CUDA(cudaFuncSetAttribute(conv_wgrad_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = a.n_mgroups * a.n_ntiles * a.ksplit;
+  const double es = sizeof(act_t);
+  const double bytes = (double)w.N * w.H * w.W * w.Cinp * es + (double)w.N * w.Ho * w.Wo * w.Coutp * es +
+                       (double)a.rows * w.Coutp * 4.0;   // algorithmic: X + dY read, dW written once
+  const double flops = 2.0 * a.rows * (double)w.Coutp * w.N * w.Ho * w.Wo;
+  prof::begin(st);
+  conv_wgrad_ts_kernel<<<grid, kWtThreads, smem, st>>>(tX, tD, a);
+  PST_CUDA(cudaGetLastError());
+  prof::end(st, prof::CONV_WGRAD, bytes, flops);
+  return true;
+}
+#else
+int wgrad_ts_ksplit(int, int, int, int, int, int, int, int, int, int, int) { return 0; }
+bool conv_wgrad_ts(const WgradSpec&, cudaStream_t) { return false; }
+#endif
+
+}  // namespace pst

@@ -54,6 +54,10 @@ struct WgradSpec {
 struct WgradPlan { int ksplit; int64_t part_floats; };
 WgradPlan wgrad_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm);
 void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st);
+// TS-mode wgrad (expanded input operand in TMEM, 3xTF32 build): false if the shape does not fit;
+// wgrad_ts_ksplit() is its split-K factor (0 if it does not apply).
+bool conv_wgrad_ts(const WgradSpec& w, cudaStream_t st);
+int wgrad_ts_ksplit(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm);
 
 // ---------------------------------------------------------------- elementwise / reductions
 // NCHW float32 -> channel-planar act_t, channels zero-padded to Cp.
