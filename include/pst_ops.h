@@ -28,6 +28,11 @@ int pst_op_conv2d_dgrad(const float* gy, const float* w, float* gx, int N, int C
                         int k, int stride, int pad);
 int pst_op_conv2d_wgrad(const float* x, const float* gy, float* gw, int N, int Cin, int H, int W, int Cout,
                         int k, int stride, int pad);
+/* Tuning aid: mean device time (microseconds, *us) of one fwd (which=0, BN-statistics
+ * epilogue), dgrad (1, stride 1) or wgrad (2) launch of this shape on resident zero buffers,
+ * `iters` launches replayed as one CUDA graph after a warm-up replay. */
+int pst_op_time_conv(int which, int N, int Cin, int H, int W, int Cout, int k, int stride, int pad,
+                     int iters, float* us);
 /* Message of the last failing pst_op_* call on this thread. */
 const char* pst_op_last_error(void);
 

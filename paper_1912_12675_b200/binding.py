@@ -94,6 +94,7 @@ def lib():
         "pst_op_conv2d_fwd": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 8),
         "pst_op_conv2d_dgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 8),
         "pst_op_conv2d_wgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 8),
+        "pst_op_time_conv": (C.c_int, [C.c_int] * 10 + [P(C.c_float)]),
         "pst_op_last_error": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -335,6 +336,12 @@ class _Ops:
         self._run(lib().pst_op_conv2d_wgrad, x.data_ptr(), gy.data_ptr(), gw.data_ptr(), N, Cin, H, W, Cout, k,
                   stride, pad)
         return gw
+
+    def time_conv(self, which, N, Cin, H, W, Cout, k, stride, pad, iters=50):
+        """Mean device microseconds of one fwd (0) / dgrad (1) / wgrad (2) launch (tuning aid)."""
+        us = C.c_float(0.0)
+        self._run(lib().pst_op_time_conv, which, N, Cin, H, W, Cout, k, stride, pad, iters, C.byref(us))
+        return us.value
 
 
 ops = _Ops()

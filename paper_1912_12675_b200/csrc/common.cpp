@@ -1,3 +1,4 @@
+#include <cstdlib>
 // common.cpp -- tensor-map encoding and device queries.
 #include "common.h"
 
@@ -106,4 +107,14 @@ void read(int cls, double* ms, int64_t* n, double* bytes, double* flops) {
 }
 }  // namespace prof
 
+}  // namespace pst
+
+namespace pst {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PST_PDL");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
 }  // namespace pst

@@ -119,6 +119,31 @@ CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void* gaddr, const
 int num_sms(int device);
 
 // Launch accounting and optional per-kernel CUDA-event timing (bench.py's roofline).
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the step is launched with the PDL attribute: its CTAs may become resident and
+// run their prologue (barrier init, TMEM alloc, descriptor prefetch) while the previous kernel
+// drains.  Kernels call pdl_wait() before their first global-memory access (read or write) and
+// pdl_trigger() right after it, so kernel N starts only once kernel N-1 has passed its own wait,
+// i.e. every kernel before N-1 is complete.  PST_PDL=0 disables the attribute (A/B timing).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 namespace prof {
 enum Cls { CONV_FWD = 0, CONV_DGRAD, CONV_WGRAD, BN_APPLY, BWD_PRE, BN_BWD, POOL, SGD, LOSS, MISC, NCLS };
 extern thread_local int64_t launches;  // kernels enqueued by this thread (graph capture included)

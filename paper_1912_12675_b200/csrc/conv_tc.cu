@@ -193,6 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
+  pdl_wait();      // no global memory access above this line
+  pdl_trigger();
   const int nch = a.kc / kEPC;   // 16-byte channel chunks per stage
 
   if (warp == 0) {
@@ -571,6 +573,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
+  pdl_wait();      // no global memory access above this line
+  pdl_trigger();
   const int n_iter = p_hi - p_lo;
 
   if (warp == 0) {
@@ -754,6 +758,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
+  pdl_wait();      // no global memory access above this line
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0 && n_iter > 0) {
@@ -1127,7 +1133,7 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
                        (c.res ? (double)c.N * c.res_H * c.res_W * c.res_C * es : 0.0);
   const double flops = 2.0 * c.N * c.Ho * c.Wo * c.Coutp * (double)c.Cinp * a.taps;
   prof::begin(st);
-  kern<<<grid, kThreads, smem, st>>>(tA, tB, tBlo, a);
+  PST_CUDA(launch_k(kern, dim3(grid), dim3(kThreads), smem, st, tA, tB, tBlo, a));
   PST_CUDA(cudaGetLastError());
   prof::end(st, c.epi == EPI_DGRAD ? prof::CONV_DGRAD : prof::CONV_FWD, bytes, flops);
 }
@@ -1248,7 +1254,7 @@ void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
                          (double)b.rows * w.Coutp * 4.0;   // algorithmic: X + dY read, dW written once
     const double flops = 2.0 * b.rows * (double)w.Coutp * w.N * w.Ho * w.Wo;
     prof::begin(st);
-    conv_wgrad_band_kernel<<<grid, kThreads, smem, st>>>(tX, tD, b);
+    PST_CUDA(launch_k(conv_wgrad_band_kernel, dim3(grid), dim3(kThreads), smem, st, tX, tD, b));
     PST_CUDA(cudaGetLastError());
     prof::end(st, prof::CONV_WGRAD, bytes, flops);
     return;
@@ -1288,7 +1294,7 @@ void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
                        (double)a.rows * w.Coutp * 4.0;   // algorithmic: X + dY read, dW written once
   const double flops = 2.0 * a.rows * (double)w.Coutp * w.N * w.Ho * w.Wo;
   prof::begin(st);
-  conv_wgrad_kernel<<<grid, kThreads, smem, st>>>(tX, tD, a);
+  PST_CUDA(launch_k(conv_wgrad_kernel, dim3(grid), dim3(kThreads), smem, st, tX, tD, a));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::CONV_WGRAD, bytes, flops);
 }

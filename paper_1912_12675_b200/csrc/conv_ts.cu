@@ -18,6 +18,7 @@
 //   warps 2-5  epilogue (BN statistics / bias+ReLU / dgrad residual), double-buffered D.
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.h"
 #include "kernels.h"
@@ -50,11 +51,12 @@ struct TsArgs {
   const act_t* res;
   int res_mode, res_H, res_W, res_C, res_pad;
   unsigned long long* dbg;   // optional timeline (CTA 0), PST_DBG_TL
+  int knob;                  // experiment switches (PST_TS_KNOB), 0 in production
 };
 
 __device__ __forceinline__ unsigned long long ts_gtime() {
   unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));   // SM cycles (globaltimer reads are slow)
   return t;
 }
 #define TSL(ev, i)                                                   \
@@ -66,7 +68,7 @@ __device__ __forceinline__ float ld_planar_f(const act_t* base, int64_t npix, in
   return act2f(base[((int64_t)(c / kEPC) * npix + pix) * kEPC + c % kEPC]);
 }
 
-template <int KC>
+template <int KC, int EPI>
 __global__ void __launch_bounds__(kTsThreads, 1)
     conv_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, const TsArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -83,6 +85,8 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* wbar = tempty + 2;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(wbar + 1);
+  int* tsh = reinterpret_cast<int*>(tmem_ptr + 4);   // tap shifts (a.tapshift indexed dynamically
+                                                     // from the param space would be copied to local memory)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TSL(7, 0);
@@ -99,13 +103,24 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(tmem_ptr, 512);
+#pragma unroll 1
+  for (int t = threadIdx.x; t < 49; t += blockDim.x) {
+    int v = 0;
+#pragma unroll
+    for (int j = 0; j < 49; ++j) v = (j == t) ? a.tapshift[j] : v;
+    tsh[t] = v;
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
+  pdl_wait();      // no global memory access above this line
+  pdl_trigger();
   const uint32_t a_col0 = 2 * a.BN;                  // accumulators: columns [0, 2 BN)
 
-  if (warp == 0) {
+  if (a.knob & 16) {
+    // experiment: prologue and teardown only
+  } else if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (ptx::elect_one()) {
       ptx::prefetch_tmap(&tmA);
@@ -129,9 +144,11 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         ptx::mbar_wait(&bempty[bs], bph ^ 1);
         if (lane == 0) TSL(0, dbg_i[0]++);
         if (ptx::elect_one()) {
+          if (a.knob & 32) { ptx::mbar_arrive(&full[bs]); } else {
           ptx::mbar_expect_tx(&full[bs], a.band_tx);
           ptx::tma_load_4d(bands + bs * a.band_bytes, &tmA, &full[bs], a.lo * kEPC, y0 * a.S + a.lo, n0,
                            kcc * (KC / kEPC));
+          }
         }
         __syncwarp();
         if (++bs == a.band_stages) { bs = 0; bph ^= 1; }
@@ -159,7 +176,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           if (lane == 0) TSL(4, dbg_i[4]++);
           if (ptx::elect_one()) {
             // one slot = tps taps x (KC hi + KC lo columns): 3 x KC/8 x tps MMAs per handshake
-            for (int i = 0; i < a.tps; ++i) {
+            for (int i = 0; i < a.tps && !(a.knob & 2); ++i) {
               const int t = gi * a.tps + i;
               const uint32_t ahi = tmem + a_col0 + (slot * a.tps + i) * 2 * KC;
               const uint64_t bt = ptx::desc_add(wdesc, t * wtap + kcc * (KC / kEPC) * (a.BN * 16));
@@ -201,16 +218,18 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     uint32_t cnt = 0;                        // global group counter (same order as the MMA issuer)
     for (int m = m0; m < a.n_mtiles; m += mstep) {
       for (int kcc = 0; kcc < a.n_kc; ++kcc) {
-        ptx::mbar_wait(&full[bs], bph);
+        if (a.knob & 128) ptx::mbar_wait_sleep(&full[bs], bph, 100); else ptx::mbar_wait(&full[bs], bph);
         const uint8_t* band = bands + bs * a.band_bytes;
         for (int gi = (int)((cnt + set) & 1); gi < ngrp; gi += 2) {
           const uint32_t c = cnt + gi;
           const int slot = (int)(c % a.n_slots);
-          ptx::mbar_wait(&aempty[slot], ((c / a.n_slots) & 1) ^ 1);
+          if (a.knob & 128) ptx::mbar_wait_sleep(&aempty[slot], ((c / a.n_slots) & 1) ^ 1, 100);
+          else ptx::mbar_wait(&aempty[slot], ((c / a.n_slots) & 1) ^ 1);
           ptx::tc_fence_after();
-          for (int i = 0; i < a.tps; ++i) {
+          if (threadIdx.x == 192) TSL(1, dbg_i[1]++);
+          for (int i = 0; i < a.tps && !(a.knob & 1); ++i) {
             const int t = gi * a.tps + i;
-            const uint8_t* src = band + (uint32_t)(pixoff + a.tapshift[t]) * 16;
+            const uint8_t* src = band + (uint32_t)(pixoff + tsh[t]) * 16;
             float hi[KC], lo[KC];
 #pragma unroll
             for (int p4 = 0; p4 < KC / 4; ++p4) {
@@ -230,6 +249,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&afull[slot]);
+          if (threadIdx.x == 192) TSL(3, dbg_i[3]++);
         }
         cnt += ngrp;
         __syncwarp();
@@ -239,16 +259,22 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 2..5)
+    // BN statistics: per 16-channel group a warp reduce-scatter leaves the sum over the warp's
+    // 32 pixels of channel (lane >> 1) in lanes lane, lane^1; the even lane accumulates it into
+    // the warp's fp64 slot in shared memory; the four warps' slots are combined at the end and
+    // written with one global atomic per channel.
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const int et = threadIdx.x - 64;         // 0..127
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    float* sw = sst + q * 32 * 17;           // this warp's 32 x 17 transpose scratch
-    double* cacc = reinterpret_cast<double*>(sst + 4 * 32 * 17);   // [BN][2] CTA partial BN sums
-    for (int i = et; i < 2 * a.BN; i += 128) cacc[i] = 0.0;
-    ptx::named_bar_sync(1, 128);
+    double* wacc = reinterpret_cast<double*>(sst);   // [4 warps][BN][2]  (<= 8 KB)
+    if (EPI == EPI_BN_STATS) {
+      for (int i = lane; i < 2 * a.BN; i += 32) wacc[q * 2 * a.BN + i] = 0.0;
+      __syncwarp();
+    }
     const int per_img = a.rows_t * a.Wo;
     const int64_t npix = (int64_t)a.N * a.Ho * a.Wo;
+    const int ng = a.BN / 16;
     int local = 0;
     for (int m = m0; m < a.n_mtiles; m += mstep, ++local) {
       const int acc = local & 1;
@@ -260,28 +286,24 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       const int x = r % a.Wo;
       const bool valid = n < a.N;
       const int64_t pix = ((int64_t)n * a.Ho + y) * a.Wo + x;
-      for (int g = 0; g < a.BN / 16; ++g) {
+      for (int g = 0; g < ng; ++g) {
         float u[16];
-        ptx::tmem_ld16(tmem + lane_addr + acc * a.BN + g * 16, u);
-        if (g == a.BN / 16 - 1) {
+        if (a.knob & 64) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) u[i] = 0.f;
+        } else ptx::tmem_ld16(tmem + lane_addr + acc * a.BN + g * 16, u);
+        if (g == ng - 1) {
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
         }
         const int c0 = nt * a.BN + g * 16;
-        if (a.epi == EPI_BN_STATS) {
+        if (EPI == EPI_BN_STATS) {
+          if (!valid) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) u[i] = valid ? act2f(f2act(u[i])) : 0.f;
-        } else if (a.epi == EPI_BIAS_ACT || a.epi == EPI_BIAS_F32) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int c = c0 + i;
-            const float b = (a.bias != nullptr && c < a.Cout) ? __ldg(&a.bias[c]) : 0.f;
-            float o = u[i] + b;
-            if (a.relu) o = fmaxf(o, 0.f);
-            u[i] = (c < a.Cout) ? o : 0.f;
+            for (int i = 0; i < 16; ++i) u[i] = 0.f;
           }
-        } else {  // EPI_DGRAD: + shortcut^T of the residual layer's gradient
+        } else if (EPI == EPI_DGRAD) {   // + shortcut^T of the residual layer's gradient
           if (valid && a.res_mode == 1) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) u[i] += ld_planar_f(a.res, npix, pix, c0 + i);
@@ -294,40 +316,55 @@ __global__ void __launch_bounds__(kTsThreads, 1)
               if (c < a.Cout) u[i] += ld_planar_f(a.res, rnpix, rpix, c + a.res_pad);
             }
           }
+        } else {                           // EPI_BIAS_ACT / EPI_BIAS_F32
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int c = c0 + i;
+            const float b = (a.bias != nullptr && c < a.Cout) ? __ldg(&a.bias[c]) : 0.f;
+            float o = u[i] + b;
+            if (a.relu) o = fmaxf(o, 0.f);
+            u[i] = (c < a.Cout) ? o : 0.f;
+          }
         }
-        if (valid) {
+        if (valid && !(a.knob & 8)) {
           float* o = reinterpret_cast<float*>(a.out);   // act_t == float in this build
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj)
             *reinterpret_cast<float4*>(o + ((int64_t)(c0 / 4 + jj) * npix + pix) * 4) =
                 make_float4(u[4 * jj], u[4 * jj + 1], u[4 * jj + 2], u[4 * jj + 3]);
         }
-        if (threadIdx.x == 64) TSL(3, dbg_i[3]++);
-        if (a.epi == EPI_BN_STATS) {
-          // per-warp transpose: lane c < 16 sums channel c over the warp's 32 pixels
+        if (EPI == EPI_BN_STATS && !(a.knob & 4)) {
+          float s1[16], s2[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) sw[lane * 17 + i] = u[i];
-          __syncwarp();
-          if (lane < 16) {
-            float t1 = 0.f, t2 = 0.f;
-#pragma unroll 8
-            for (int p = 0; p < 32; ++p) {
-              const float z = sw[p * 17 + lane];
-              t1 += z;
-              t2 += z * z;
+          for (int i = 0; i < 16; ++i) { s1[i] = u[i]; s2[i] = u[i] * u[i]; }
+#pragma unroll
+          for (int w = 8; w >= 1; w >>= 1) {       // 16 -> 8 -> 4 -> 2 -> 1 values per lane
+            const bool up = (lane & (2 * w)) != 0;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+              const float t1 = up ? s1[i] : s1[i + w], k1 = up ? s1[i + w] : s1[i];
+              const float t2 = up ? s2[i] : s2[i + w], k2 = up ? s2[i + w] : s2[i];
+              s1[i] = k1 + __shfl_xor_sync(0xffffffffu, t1, 2 * w);
+              s2[i] = k2 + __shfl_xor_sync(0xffffffffu, t2, 2 * w);
             }
-            atomicAdd(&cacc[2 * (g * 16 + lane)], (double)t1);
-            atomicAdd(&cacc[2 * (g * 16 + lane) + 1], (double)t2);
           }
-          __syncwarp();
+          s1[0] += __shfl_xor_sync(0xffffffffu, s1[0], 1);   // lanes 2c, 2c+1 hold channel c
+          s2[0] += __shfl_xor_sync(0xffffffffu, s2[0], 1);
+          if ((lane & 1) == 0) {
+            double* w2 = wacc + q * 2 * a.BN + 2 * (g * 16 + (lane >> 1));
+            w2[0] += (double)s1[0];
+            w2[1] += (double)s2[0];
+          }
         }
       }
       if (threadIdx.x == 64) TSL(6, dbg_i[6]++);
     }
-    if (a.epi == EPI_BN_STATS) {
+    if (EPI == EPI_BN_STATS) {
       ptx::named_bar_sync(1, 128);
-      for (int i = et; i < 2 * a.BN; i += 128)
-        if (cacc[i] != 0.0) atomicAdd(&a.stats[2 * nt * a.BN + i], cacc[i]);
+      for (int i = et; i < 2 * a.BN; i += 128) {
+        const double v = wacc[i] + wacc[2 * a.BN + i] + wacc[4 * a.BN + i] + wacc[6 * a.BN + i];
+        if (v != 0.0) atomicAdd(&a.stats[2 * nt * a.BN + i], v);
+      }
     }
   }
   ptx::tc_fence_before();
@@ -373,7 +410,7 @@ static bool ts_plan(const ConvSpec& c, TsArgs& a, int& kc) {
   if (a.BN == 0) return false;
   a.n_ntiles = c.Coutp / a.BN;
   a.w_bytes = (uint32_t)a.taps * c.Cinp * a.BN * 4;
-  const int fixed = 2 * (int)a.w_bytes + 4 * 32 * 17 * 4 + 2048 + (2 * kMaxBand + 2 * kMaxSlots + 5) * 8 + 16;
+  const int fixed = 2 * (int)a.w_bytes + 4 * 32 * 17 * 4 + 2048 + (2 * kMaxBand + 2 * kMaxSlots + 5) * 8 + 16 + 256;
   a.band_stages = std::min(kMaxBand, (227 * 1024 - 1024 - fixed) / (int)a.band_bytes);
   if (a.band_stages < 2) return false;
   a.tps = 1;
@@ -392,6 +429,7 @@ bool conv_ts(const ConvSpec& c, cudaStream_t st) {
   a.res = c.res; a.res_mode = c.res_mode; a.res_H = c.res_H; a.res_W = c.res_W; a.res_C = c.res_C;
   a.res_pad = c.res_pad;
   a.dbg = c.dbg;
+  { static const char* kn = std::getenv("PST_TS_KNOB"); a.knob = kn ? std::atoi(kn) : 0; }
   // band box: (Wb*EPC, Hb, nb images, KC/EPC planes) of the planar input, zero outside
   uint64_t dims[4] = {(uint64_t)c.W * kEPC, (uint64_t)c.H, (uint64_t)c.N, (uint64_t)c.Cinp / kEPC};
   uint64_t str[3] = {(uint64_t)c.W * 16, (uint64_t)c.H * c.W * 16, (uint64_t)c.N * c.H * c.W * 16};
@@ -412,8 +450,14 @@ bool conv_ts(const ConvSpec& c, cudaStream_t st) {
     tW = make_tmap(act_tmap_dtype(), 4, c.wshadow, wd, ws, wb, nullptr);
   }
   const size_t smem = 2 * (size_t)a.w_bytes + (size_t)a.band_stages * a.band_bytes + 4 * 32 * 17 * 4 + 2048 +
-                      (2 * kMaxBand + 2 * kMaxSlots + 5) * 8 + 16;
-  auto kern = kc == 32 ? conv_ts_kernel<32> : conv_ts_kernel<16>;
+                      (2 * kMaxBand + 2 * kMaxSlots + 5) * 8 + 16 + 256;
+  auto pick = [&](auto kcc) {
+    constexpr int K = decltype(kcc)::value;
+    return c.epi == EPI_BN_STATS ? conv_ts_kernel<K, EPI_BN_STATS>
+         : c.epi == EPI_DGRAD    ? conv_ts_kernel<K, EPI_DGRAD>
+                                 : conv_ts_kernel<K, EPI_BIAS_ACT>;
+  };
+  auto kern = kc == 32 ? pick(std::integral_constant<int, 32>{}) : pick(std::integral_constant<int, 16>{});
   PST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev;
   PST_CUDA(cudaGetDevice(&dev));
@@ -427,7 +471,7 @@ bool conv_ts(const ConvSpec& c, cudaStream_t st) {
                        (c.res ? (double)c.N * c.res_H * c.res_W * c.res_C * es : 0.0);
   const double flops = 2.0 * c.N * c.Ho * c.Wo * c.Coutp * (double)c.Cinp * a.taps;
   prof::begin(st);
-  kern<<<grid, kTsThreads, smem, st>>>(tA, tW, a);
+  PST_CUDA(launch_k(kern, dim3(grid), dim3(kTsThreads), smem, st, tA, tW, a));
   PST_CUDA(cudaGetLastError());
   prof::end(st, c.epi == EPI_DGRAD ? prof::CONV_DGRAD : prof::CONV_FWD, bytes, flops);
   return true;

@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(kWtThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
+  pdl_wait();      // no global memory access above this line
+  pdl_trigger();
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -343,7 +345,7 @@ bool conv_wgrad_ts(const WgradSpec& w, cudaStream_t st) {
                        (double)a.rows * w.Coutp * 4.0;   // algorithmic: X + dY read, dW written once
   const double flops = 2.0 * a.rows * (double)w.Coutp * w.N * w.Ho * w.Wo;
   prof::begin(st);
-  conv_wgrad_ts_kernel<<<grid, kWtThreads, smem, st>>>(tX, tD, a);
+  PST_CUDA(launch_k(conv_wgrad_ts_kernel, dim3(grid), dim3(kWtThreads), smem, st, tX, tD, a));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::CONV_WGRAD, bytes, flops);
   return true;

@@ -42,6 +42,8 @@ int grid_for(int64_t work, int per_block = kBlock) {
 // ------------------------------------------------------------------ layout conversion
 __global__ void nchw_to_act_kernel(const float* __restrict__ x, act_t* __restrict__ out, int N, int C, int H,
                                    int W, int Cp) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t npix = (int64_t)N * H * W;
   const int64_t nvec = npix * (Cp / E);
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
@@ -60,6 +62,8 @@ __global__ void nchw_to_act_kernel(const float* __restrict__ x, act_t* __restric
 }
 
 __global__ void act_to_nchw_kernel(const void* in, int in_f32, float* out, int N, int C, int H, int W) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t n_el = (int64_t)N * C * H * W;
   const int64_t npix = (int64_t)N * H * W;
   const int e = in_f32 ? 4 : E;
@@ -75,70 +79,104 @@ __global__ void act_to_nchw_kernel(const void* in, int in_f32, float* out, int N
 }
 
 // ------------------------------------------------------------------ BN forward apply
+// grid (x = pixel chunks of kU*kBlock vectors, y = channel plane): 32-bit pixel indices, the
+// plane's 4 scale/shift pairs in registers, kU independent 16-byte loads in flight per thread.
+constexpr int kU = 4;
 __global__ void bn_apply_kernel(const BnApplySpec s) {
-  extern __shared__ float sh[];  // scale[Cp], shift[Cp]
-  float* scale = sh;
-  float* shift = sh + s.Cp;
-  const int64_t npix = (int64_t)s.N * s.H * s.W;
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float sc[2 * E];
+  const int plane = blockIdx.y;
+  const int c0 = plane * E;
+  const int npix = s.N * s.H * s.W;
   const double M = (double)npix;
-  for (int c = threadIdx.x; c < s.Cp; c += blockDim.x) {
+  if (threadIdx.x < E) {
+    const int c = c0 + threadIdx.x;
+    float scale = 0.f, shift = 0.f;
     if (c < s.C) {
       const double mean = s.stats[2 * c] / M;
       double var = s.stats[2 * c + 1] / M - mean * mean;
       var = var < 0.0 ? 0.0 : var;
       const float invstd = (float)(1.0 / sqrt(var + (double)s.eps));
       const float g = s.gamma[c], b = s.beta[c];
-      scale[c] = g * invstd;
-      shift[c] = b - (float)mean * g * invstd;
+      scale = g * invstd;
+      shift = b - (float)mean * g * invstd;
       if (blockIdx.x == 0) {
         s.saved[2 * c] = (float)mean;
         s.saved[2 * c + 1] = invstd;
         s.run_mean[c] = (1.f - s.momentum) * s.run_mean[c] + s.momentum * (float)mean;
         s.run_var[c] = (1.f - s.momentum) * s.run_var[c] + s.momentum * (float)(var * M / (M - 1.0));
       }
-    } else {
-      scale[c] = 0.f;
-      shift[c] = 0.f;
     }
+    sc[threadIdx.x] = scale;
+    sc[E + threadIdx.x] = shift;
   }
   __syncthreads();
-  const int64_t nvec = npix * (s.Cp / E);
-  const int64_t rnpix = (int64_t)s.N * s.res_H * s.res_W;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
-    const int plane = (int)(v / npix);
-    const int64_t p = v % npix;
-    const int c0 = plane * E;
-    float f[E];
-    ldv(s.y + v * E, f);
+  float scale[E], shift[E];
 #pragma unroll
-    for (int j = 0; j < E; ++j) f[j] = f[j] * scale[c0 + j] + shift[c0 + j];
+  for (int j = 0; j < E; ++j) { scale[j] = sc[j]; shift[j] = sc[E + j]; }
+  const act_t* yp = s.y + (size_t)plane * npix * E;
+  act_t* zp = s.z + (size_t)plane * npix * E;
+  const int rnpix = s.N * s.res_H * s.res_W;
+  const int HW = s.H * s.W;
+  for (int base = blockIdx.x * (kU * kBlock); base < npix; base += gridDim.x * (kU * kBlock)) {
+    float f[kU][E];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int p = base + u * kBlock + threadIdx.x;
+      if (p < npix) ldv(yp + (size_t)p * E, f[u]);
+    }
     if (s.res_mode == 1) {
-      float r[E];
-      ldv(s.res + v * E, r);
+      const act_t* rp = s.res + (size_t)plane * npix * E;
+      float r[kU][E];
 #pragma unroll
-      for (int j = 0; j < E; ++j) f[j] += (c0 + j < s.C) ? r[j] : 0.f;
-    } else if (s.res_mode == 2) {
-      const int n = (int)(p / ((int64_t)s.H * s.W));
-      const int hw = (int)(p % ((int64_t)s.H * s.W));
-      const int y = hw / s.W, x = hw % s.W;
-      const int64_t rp = ((int64_t)n * s.res_H + 2 * y) * s.res_W + 2 * x;
+      for (int u = 0; u < kU; ++u) {
+        const int p = base + u * kBlock + threadIdx.x;
+        if (p < npix) ldv(rp + (size_t)p * E, r[u]);
+      }
 #pragma unroll
-      for (int j = 0; j < E; ++j) {
-        const int cr = c0 + j - s.res_pad;
-        if (cr >= 0 && cr < s.res_Creal) f[j] += act2f(s.res[((int64_t)(cr / E) * rnpix + rp) * E + cr % E]);
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int j = 0; j < E; ++j) f[u][j] = f[u][j] * scale[j] + shift[j] + ((c0 + j < s.C) ? r[u][j] : 0.f);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int j = 0; j < E; ++j) f[u][j] = f[u][j] * scale[j] + shift[j];
+      if (s.res_mode == 2) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int p = base + u * kBlock + threadIdx.x;
+          if (p >= npix) continue;
+          const int n = p / HW, hw = p - n * HW;
+          const int y = hw / s.W, x = hw - y * s.W;
+          const int rp = (n * s.res_H + 2 * y) * s.res_W + 2 * x;
+#pragma unroll
+          for (int j = 0; j < E; ++j) {
+            const int cr = c0 + j - s.res_pad;
+            if (cr >= 0 && cr < s.res_Creal) f[u][j] += act2f(s.res[((size_t)(cr / E) * rnpix + rp) * E + cr % E]);
+          }
+        }
       }
     }
-    if (s.relu) {
 #pragma unroll
-      for (int j = 0; j < E; ++j) f[j] = fmaxf(f[j], 0.f);
+    for (int u = 0; u < kU; ++u) {
+      const int p = base + u * kBlock + threadIdx.x;
+      if (p >= npix) continue;
+      if (s.relu) {
+#pragma unroll
+        for (int j = 0; j < E; ++j) f[u][j] = fmaxf(f[u][j], 0.f);
+      }
+      stv(zp + (size_t)p * E, f[u]);
     }
-    stv(s.z + v * E, f);
   }
 }
 
 // ------------------------------------------------------------------ pooling
 __global__ void maxpool2_kernel(const act_t* __restrict__ in, act_t* __restrict__ out, uint8_t* __restrict__ arg,
                                 int N, int H, int W, int Cp) {
+  pdl_wait();
+  pdl_trigger();
   const int Ho = H / 2, Wo = W / 2;
   const int64_t npo = (int64_t)N * Ho * Wo, npi = (int64_t)N * H * W;
   const int64_t nvec = npo * (Cp / E);
@@ -169,6 +207,8 @@ __global__ void maxpool2_kernel(const act_t* __restrict__ in, act_t* __restrict_
 }
 
 __global__ void gap_kernel(const act_t* __restrict__ in, act_t* __restrict__ out, int N, int H, int W, int Cp) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t nvec = (int64_t)N * (Cp / E);
   const int HW = H * W;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
@@ -189,12 +229,14 @@ __global__ void gap_kernel(const act_t* __restrict__ in, act_t* __restrict__ out
 }
 
 // ------------------------------------------------------------------ backward pre (pool^T, relu^T, sums)
-// grid: (x = pixel blocks, y = channel plane).  All threads of a block share one plane.
+// grid: (x = pixel chunks, y = channel plane).  All threads of a block share one plane.
 __global__ void bwd_pre_kernel(const BwdPreSpec s) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[kBlock / 32][2 * E];
   const int plane = blockIdx.y;
   const int c0 = plane * E;
-  const int64_t npix = (int64_t)s.N * s.H * s.W;
+  const int npix = s.N * s.H * s.W;
   const int HW = s.H * s.W;
   float mean[E], inv[E], a1[E], a2[E];
 #pragma unroll
@@ -203,59 +245,85 @@ __global__ void bwd_pre_kernel(const BwdPreSpec s) {
     inv[j] = s.bn ? s.saved[2 * (c0 + j) + 1] : 0.f;
     a1[j] = a2[j] = 0.f;
   }
-  const int64_t pbase = (int64_t)plane * npix;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = pbase + p;
-    float g[E];
-    if (s.pool == 0) {
-      if (s.gout_f32) {
-        // float tensors use 4-channel planes: [Cp/4][npix][4]
-        const float* gp = reinterpret_cast<const float*>(s.gout);
+  const size_t pb = (size_t)plane * npix;
+  const int Ho2 = s.H / 2, Wo2 = s.W / 2;
+  const int npo = s.N * Ho2 * Wo2;
+  for (int base = blockIdx.x * (kU * kBlock); base < npix; base += gridDim.x * (kU * kBlock)) {
+    float g[kU][E];
 #pragma unroll
-        for (int j = 0; j < E; ++j) {
-          const int c = c0 + j;
-          g[j] = gp[((int64_t)(c >> 2) * npix + p) * 4 + (c & 3)];
+    for (int u = 0; u < kU; ++u) {
+      const int p = base + u * kBlock + threadIdx.x;
+#pragma unroll
+      for (int j = 0; j < E; ++j) g[u][j] = 0.f;
+      if (p >= npix) continue;
+      if (s.pool == 0) {
+        if (s.gout_f32) {   // float tensors use 4-channel planes: [Cp/4][npix][4]
+          const float* gp = reinterpret_cast<const float*>(s.gout);
+#pragma unroll
+          for (int j = 0; j < E; ++j) {
+            const int c = c0 + j;
+            g[u][j] = gp[((size_t)(c >> 2) * npix + p) * 4 + (c & 3)];
+          }
+        } else {
+          ldv(s.gout + (pb + p) * E, g[u]);
         }
+      } else if (s.pool == 1) {
+        const int n = p / HW, hw = p - n * HW;
+        const int y = hw / s.W, x = hw - y * s.W;
+        const size_t vo = (size_t)plane * npo + (n * Ho2 + (y >> 1)) * Wo2 + (x >> 1);
+        float gg[E];
+        ldv(s.gout + vo * E, gg);
+        const uint8_t q = (uint8_t)(((y & 1) << 1) | (x & 1));
+#pragma unroll
+        for (int j = 0; j < E; ++j) g[u][j] = (s.arg[vo * E + j] == q) ? gg[j] : 0.f;
       } else {
-        ldv(s.gout + v * E, g);
+        const int n = p / HW;
+        float gg[E];
+        ldv(s.gout + ((size_t)plane * s.N + n) * E, gg);
+#pragma unroll
+        for (int j = 0; j < E; ++j) g[u][j] = gg[j] / (float)HW;
       }
-    } else if (s.pool == 1) {
-      const int n = (int)(p / HW), hw = (int)(p % HW);
-      const int y = hw / s.W, x = hw % s.W;
-      const int64_t npo = (int64_t)s.N * (s.H / 2) * (s.W / 2);
-      const int64_t vo = (int64_t)plane * npo + ((int64_t)n * (s.H / 2) + y / 2) * (s.W / 2) + x / 2;
-      float gg[E];
-      ldv(s.gout + vo * E, gg);
-      const uint8_t q = (uint8_t)(((y & 1) << 1) | (x & 1));
-#pragma unroll
-      for (int j = 0; j < E; ++j) g[j] = (s.arg[vo * E + j] == q) ? gg[j] : 0.f;
-    } else {
-      const int n = (int)(p / HW);
-      float gg[E];
-      ldv(s.gout + ((int64_t)plane * s.N + n) * E, gg);
-#pragma unroll
-      for (int j = 0; j < E; ++j) g[j] = gg[j] / (float)HW;
     }
     if (s.relu) {
-      float z[E];
-      ldv(s.z + v * E, z);
+      float z[kU][E];
 #pragma unroll
-      for (int j = 0; j < E; ++j) g[j] = z[j] > 0.f ? g[j] : 0.f;
+      for (int u = 0; u < kU; ++u) {
+        const int p = base + u * kBlock + threadIdx.x;
+        if (p < npix) ldv(s.z + (pb + p) * E, z[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int p = base + u * kBlock + threadIdx.x;
+        if (p >= npix) continue;
+#pragma unroll
+        for (int j = 0; j < E; ++j) g[u][j] = z[u][j] > 0.f ? g[u][j] : 0.f;
+      }
+    }
+    float y[kU][E];
+    if (s.bn) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int p = base + u * kBlock + threadIdx.x;
+        if (p < npix) ldv(s.y + (pb + p) * E, y[u]);
+      }
     }
 #pragma unroll
-    for (int j = 0; j < E; ++j) g[j] = act2f(f2act(g[j]));  // sums use exactly what is stored
-    stv(s.gpre + v * E, g);
-    if (s.bn) {
-      float y[E];
-      ldv(s.y + v * E, y);
+    for (int u = 0; u < kU; ++u) {
+      const int p = base + u * kBlock + threadIdx.x;
+      if (p >= npix) continue;
 #pragma unroll
-      for (int j = 0; j < E; ++j) {
-        a1[j] += g[j];
-        a2[j] += g[j] * (y[j] - mean[j]) * inv[j];
+      for (int j = 0; j < E; ++j) g[u][j] = act2f(f2act(g[u][j]));  // sums use exactly what is stored
+      stv(s.gpre + (pb + p) * E, g[u]);
+      if (s.bn) {
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          a1[j] += g[u][j];
+          a2[j] += g[u][j] * (y[u][j] - mean[j]) * inv[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < E; ++j) a1[j] += g[u][j];
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < E; ++j) a1[j] += g[j];
     }
   }
   // block reduction (one plane per block)
@@ -285,44 +353,61 @@ __global__ void bwd_pre_kernel(const BwdPreSpec s) {
 }
 
 __global__ void bn_bwd_apply_kernel(const BnBwdSpec s) {
-  extern __shared__ float sh[];  // k1, m1, m2, mean, inv  [5][Cp]
-  float* k1 = sh;
-  float* m1 = sh + s.Cp;
-  float* m2 = sh + 2 * s.Cp;
-  float* mu = sh + 3 * s.Cp;
-  float* iv = sh + 4 * s.Cp;
-  const int64_t npix = (int64_t)s.N * s.H * s.W;
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float co[5 * E];   // k1, m1, m2, mean, invstd of the plane's channels
+  const int plane = blockIdx.y;
+  const int c0 = plane * E;
+  const int npix = s.N * s.H * s.W;
   const double M = (double)npix;
-  for (int c = threadIdx.x; c < s.Cp; c += blockDim.x) {
+  if (threadIdx.x < E) {
+    const int c = c0 + threadIdx.x;
+    float k1 = 0.f, m1 = 0.f, m2 = 0.f, mu = 0.f, iv = 0.f;
     if (c < s.C) {
-      mu[c] = s.saved[2 * c];
-      iv[c] = s.saved[2 * c + 1];
-      k1[c] = s.gamma[c] * iv[c];
-      m1[c] = (float)(s.sums[2 * c] / M);
-      m2[c] = (float)(s.sums[2 * c + 1] / M);
-    } else {
-      mu[c] = iv[c] = k1[c] = m1[c] = m2[c] = 0.f;
+      mu = s.saved[2 * c];
+      iv = s.saved[2 * c + 1];
+      k1 = s.gamma[c] * iv;
+      m1 = (float)(s.sums[2 * c] / M);
+      m2 = (float)(s.sums[2 * c + 1] / M);
     }
+    co[threadIdx.x] = k1; co[E + threadIdx.x] = m1; co[2 * E + threadIdx.x] = m2;
+    co[3 * E + threadIdx.x] = mu; co[4 * E + threadIdx.x] = iv;
   }
   __syncthreads();
-  const int64_t nvec = npix * (s.Cp / E);
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(v / npix) * E;
-    float g[E], y[E], o[E];
-    ldv(s.gpre + v * E, g);
-    ldv(s.y + v * E, y);
+  float k1[E], m1[E], m2[E], mu[E], iv[E];
 #pragma unroll
-    for (int j = 0; j < E; ++j) {
-      const int c = c0 + j;
-      const float xh = (y[j] - mu[c]) * iv[c];
-      o[j] = k1[c] * (g[j] - m1[c] - xh * m2[c]);
+  for (int j = 0; j < E; ++j) {
+    k1[j] = co[j]; m1[j] = co[E + j]; m2[j] = co[2 * E + j]; mu[j] = co[3 * E + j]; iv[j] = co[4 * E + j];
+  }
+  const act_t* gp = s.gpre + (size_t)plane * npix * E;
+  const act_t* yp = s.y + (size_t)plane * npix * E;
+  act_t* op = s.gy + (size_t)plane * npix * E;
+  for (int base = blockIdx.x * (kU * kBlock); base < npix; base += gridDim.x * (kU * kBlock)) {
+    float g[kU][E], y[kU][E];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int p = base + u * kBlock + threadIdx.x;
+      if (p < npix) { ldv(gp + (size_t)p * E, g[u]); ldv(yp + (size_t)p * E, y[u]); }
     }
-    stv(s.gy + v * E, o);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int p = base + u * kBlock + threadIdx.x;
+      if (p >= npix) continue;
+      float o[E];
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const float xh = (y[u][j] - mu[j]) * iv[j];
+        o[j] = k1[j] * (g[u][j] - m1[j] - xh * m2[j]);
+      }
+      stv(op + (size_t)p * E, o);
+    }
   }
 }
 
 __global__ void dilate2_kernel(const act_t* __restrict__ dy, act_t* __restrict__ out, int N, int Ho, int Wo,
                                int H, int W, int Cp) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t npo = (int64_t)N * Ho * Wo, npi = (int64_t)N * H * W;
   const int64_t nvec = npi * (Cp / E);
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
@@ -343,6 +428,8 @@ __global__ void dilate2_kernel(const act_t* __restrict__ dy, act_t* __restrict__
 __global__ void softmax_ce_kernel(const float* __restrict__ logits, const int32_t* __restrict__ label_ring, int ring,
                                   float* __restrict__ loss_ring, int64_t* fwd_counter, float* __restrict__ dz, int B,
                                   int C, int Cp) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float wsum[32];
   const int64_t f = *fwd_counter;
   const int32_t* labels = label_ring + (f % ring) * B;
@@ -386,6 +473,8 @@ __device__ __forceinline__ int64_t shb_idx(int tap, int co, int ci, int Coutp, i
 
 template <bool kUpdate>
 __global__ void sgd_kernel(const SgdSpec s) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float lr_sh;
   __shared__ int seg_sh;
   __shared__ int last_sh;
@@ -423,9 +512,8 @@ __global__ void sgd_kernel(const SgdSpec s) {
       if (g.kind == SEG_VEC) {
         grad = (float)g.src_d[2 * e + g.comp];
       } else {
-        const int64_t rows = (int64_t)g.k * g.k * g.Cinp;
         const int64_t row = (int64_t)tap * g.Cinp + ci;
-        for (int ks = 0; ks < g.ksplit; ++ks) grad += g.part[((int64_t)ks * rows + row) * g.Coutp + co];
+        grad = g.gsum[row * g.Coutp + co];
       }
       float v = s.v[g.off + e];
       v = s.momentum * v + (grad + s.wd * w);
@@ -462,8 +550,38 @@ __global__ void sgd_kernel(const SgdSpec s) {
   }
 }
 
+// Split-K reduction of every conv segment's wgrad partials: gsum[i] = sum_ks part[ks][i], one
+// float4 per thread, coalesced in the partials' own [rows][Coutp] order.
+__global__ void wgrad_sum_kernel(const SgdSpec s) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int seg_sh;
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = s.n_segs - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (s.red_block_start[mid] <= blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    seg_sh = lo;
+  }
+  __syncthreads();
+  const SgdSeg& g = s.segs[seg_sh];
+  const int64_t nv = (int64_t)g.k * g.k * g.Cinp * g.Coutp / 4;
+  const int64_t i = (int64_t)(blockIdx.x - s.red_block_start[seg_sh]) * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const float4* p = reinterpret_cast<const float4*>(g.part) + i;
+  float4 a = __ldg(p);
+  for (int ks = 1; ks < g.ksplit; ++ks) {
+    const float4 b = __ldg(p + (int64_t)ks * nv);
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+  }
+  reinterpret_cast<float4*>(g.gsum)[i] = a;
+}
+
 __global__ void conv_w_shadow_kernel(const float* w, int cout, int cin, int k, int Coutp, int Cinp, act_t* sf,
                                      act_t* sb) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t n = (int64_t)cout * cin * k * k;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int kk = k * k;
@@ -485,6 +603,8 @@ __global__ void conv_w_shadow_kernel(const float* w, int cout, int cin, int k, i
 
 __global__ void wgrad_reduce_kernel(const float* part, int ksplit, int Coutp, int Cinp, int cout, int cin, int k,
                                     float* out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t n = (int64_t)cout * cin * k * k;
   const int64_t rows = (int64_t)k * k * Cinp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -501,23 +621,32 @@ __global__ void wgrad_reduce_kernel(const float* part, int ksplit, int Coutp, in
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+// pixel-chunk grid for the plane-blocked kernels: about 4 resident blocks per SM in total
+static dim3 plane_grid(int npix, int planes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int want = std::max(1, num_sms(dev) * 4 / planes);
+  const int chunks = (npix + kU * kBlock - 1) / (kU * kBlock);
+  return dim3((unsigned)std::max(1, std::min(chunks, want)), (unsigned)planes);
+}
+
 void input_to_act(const float* x, act_t* out, int N, int C, int H, int W, int Cp, cudaStream_t st) {
   const int64_t nvec = (int64_t)N * H * W * (Cp / E);
   prof::begin(st);
-  nchw_to_act_kernel<<<grid_for(nvec), kBlock, 0, st>>>(x, out, N, C, H, W, Cp);
+  PST_CUDA(launch_k(nchw_to_act_kernel, dim3(grid_for(nvec)), dim3(kBlock), 0, st, x, out, N, C, H, W, Cp));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::MISC, (double)N * H * W * (C * 4.0 + Cp * sizeof(act_t)), 0);
 }
 
 void act_to_nchw(const void* in, int in_f32, float* out, int N, int C, int H, int W, cudaStream_t st) {
-  act_to_nchw_kernel<<<grid_for((int64_t)N * C * H * W), kBlock, 0, st>>>(in, in_f32, out, N, C, H, W);
+  PST_CUDA(launch_k(act_to_nchw_kernel, dim3(grid_for((int64_t)N * C * H * W)), dim3(kBlock), 0, st, in, in_f32, out, N, C, H, W));
   PST_CUDA(cudaGetLastError());
 }
 
 void bn_apply(const BnApplySpec& s, cudaStream_t st) {
   const int64_t nvec = (int64_t)s.N * s.H * s.W * (s.Cp / E);
   prof::begin(st);
-  bn_apply_kernel<<<grid_for(nvec), kBlock, 2 * s.Cp * sizeof(float), st>>>(s);
+  PST_CUDA(launch_k(bn_apply_kernel, plane_grid(s.N * s.H * s.W, s.Cp / E), dim3(kBlock), 0, st, s));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::BN_APPLY, (double)nvec * 16 * (s.res_mode ? 3 : 2), 0);
 }
@@ -526,7 +655,7 @@ void maxpool2_fwd(const act_t* in, act_t* out, uint8_t* arg, int N, int H, int W
   PST_CHECK_ARG(H % 2 == 0 && W % 2 == 0, "maxpool2 needs even H, W");
   const int64_t nvec = (int64_t)N * (H / 2) * (W / 2) * (Cp / E);
   prof::begin(st);
-  maxpool2_kernel<<<grid_for(nvec), kBlock, 0, st>>>(in, out, arg, N, H, W, Cp);
+  PST_CUDA(launch_k(maxpool2_kernel, dim3(grid_for(nvec)), dim3(kBlock), 0, st, in, out, arg, N, H, W, Cp));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::POOL, (double)nvec * (16 * 5 + E), 0);
 }
@@ -534,7 +663,7 @@ void maxpool2_fwd(const act_t* in, act_t* out, uint8_t* arg, int N, int H, int W
 void gap_fwd(const act_t* in, act_t* out, int N, int H, int W, int Cp, cudaStream_t st) {
   const int64_t nvec = (int64_t)N * (Cp / E);
   prof::begin(st);
-  gap_kernel<<<grid_for(nvec), kBlock, 0, st>>>(in, out, N, H, W, Cp);
+  PST_CUDA(launch_k(gap_kernel, dim3(grid_for(nvec)), dim3(kBlock), 0, st, in, out, N, H, W, Cp));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::POOL, (double)nvec * 16 * (H * W + 1), 0);
 }
@@ -544,10 +673,9 @@ void bwd_pre(const BwdPreSpec& s, cudaStream_t st) {
   const int planes = s.Cp / E;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int want = std::max(1, num_sms(dev) * 4 / planes);
-  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((npix + kBlock - 1) / kBlock, want));
+  (void)dev;
   prof::begin(st);
-  bwd_pre_kernel<<<dim3(gx, planes), kBlock, 0, st>>>(s);
+  PST_CUDA(launch_k(bwd_pre_kernel, plane_grid((int)npix, planes), dim3(kBlock), 0, st, s));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::BWD_PRE, (double)npix * planes * 16 * (2 + (s.relu ? 1 : 0) + (s.bn ? 1 : 0)), 0);
 }
@@ -555,7 +683,7 @@ void bwd_pre(const BwdPreSpec& s, cudaStream_t st) {
 void bn_bwd_apply(const BnBwdSpec& s, cudaStream_t st) {
   const int64_t nvec = (int64_t)s.N * s.H * s.W * (s.Cp / E);
   prof::begin(st);
-  bn_bwd_apply_kernel<<<grid_for(nvec), kBlock, 5 * s.Cp * sizeof(float), st>>>(s);
+  PST_CUDA(launch_k(bn_bwd_apply_kernel, plane_grid(s.N * s.H * s.W, s.Cp / E), dim3(kBlock), 0, st, s));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::BN_BWD, (double)nvec * 16 * 3, 0);
 }
@@ -563,7 +691,7 @@ void bn_bwd_apply(const BnBwdSpec& s, cudaStream_t st) {
 void dilate2(const act_t* dy, act_t* dyd, int N, int Ho, int Wo, int H, int W, int Cp, cudaStream_t st) {
   const int64_t nvec = (int64_t)N * H * W * (Cp / E);
   prof::begin(st);
-  dilate2_kernel<<<grid_for(nvec), kBlock, 0, st>>>(dy, dyd, N, Ho, Wo, H, W, Cp);
+  PST_CUDA(launch_k(dilate2_kernel, dim3(grid_for(nvec)), dim3(kBlock), 0, st, dy, dyd, N, Ho, Wo, H, W, Cp));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::MISC, (double)nvec * 16 * 1.25, 0);
 }
@@ -571,33 +699,35 @@ void dilate2(const act_t* dy, act_t* dyd, int N, int Ho, int Wo, int H, int W, i
 void softmax_ce(const float* logits, const int32_t* label_ring, int ring, float* loss_ring, int64_t* fwd_counter,
                 float* dz, int B, int C, int Cp, cudaStream_t st) {
   prof::begin(st);
-  softmax_ce_kernel<<<1, 512, 0, st>>>(logits, label_ring, ring, loss_ring, fwd_counter, dz, B, C, Cp);
+  PST_CUDA(launch_k(softmax_ce_kernel, dim3(1), dim3(512), 0, st, logits, label_ring, ring, loss_ring, fwd_counter, dz, B, C, Cp));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::LOSS, (double)B * Cp * 8.0, 0);
 }
 
 void sgd_update(const SgdSpec& s, cudaStream_t st) {
   prof::begin(st);
-  sgd_kernel<true><<<(unsigned)s.total_blocks, kBlock, 0, st>>>(s);
+  PST_CUDA(launch_k(wgrad_sum_kernel, dim3((unsigned)s.red_total_blocks), dim3(kBlock), 0, st, s));
+  PST_CUDA(cudaGetLastError());
+  PST_CUDA(launch_k(sgd_kernel<true>, dim3((unsigned)s.total_blocks), dim3(kBlock), 0, st, s));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::SGD, (double)s.total_blocks * kBlock * 4.0 * 5, 0);
 }
 
 void build_shadows(const SgdSpec& s, cudaStream_t st) {
-  sgd_kernel<false><<<(unsigned)s.total_blocks, kBlock, 0, st>>>(s);
+  PST_CUDA(launch_k(sgd_kernel<false>, dim3((unsigned)s.total_blocks), dim3(kBlock), 0, st, s));
   PST_CUDA(cudaGetLastError());
 }
 
 void conv_weights_to_shadows(const float* w, int cout, int cin, int k, int Coutp, int Cinp, act_t* sf, act_t* sb,
                              cudaStream_t st) {
-  conv_w_shadow_kernel<<<grid_for((int64_t)cout * cin * k * k), kBlock, 0, st>>>(w, cout, cin, k, Coutp, Cinp, sf, sb);
+  PST_CUDA(launch_k(conv_w_shadow_kernel, dim3(grid_for((int64_t)cout * cin * k * k)), dim3(kBlock), 0, st, w, cout, cin, k, Coutp, Cinp, sf, sb));
   PST_CUDA(cudaGetLastError());
 }
 
 void wgrad_reduce(const float* part, int ksplit, int Coutp, int Cinp, int cout, int cin, int k, float* out,
                   cudaStream_t st) {
-  wgrad_reduce_kernel<<<grid_for((int64_t)cout * cin * k * k), kBlock, 0, st>>>(part, ksplit, Coutp, Cinp, cout, cin,
-                                                                               k, out);
+  PST_CUDA(launch_k(wgrad_reduce_kernel, dim3(grid_for((int64_t)cout * cin * k * k)), dim3(kBlock), 0, st, part, ksplit, Coutp, Cinp, cout, cin,
+                                                                               k, out));
   PST_CUDA(cudaGetLastError());
 }
 

@@ -135,6 +135,7 @@ struct SgdSeg {
   int cout, cin, k;         // canonical dims
   int Coutp, Cinp;          // padded GEMM dims
   const float* part; int ksplit;  // wgrad partials [ksplit][k*k*Cinp][Coutp]
+  float* gsum;              // reduced gradient [k*k*Cinp][Coutp] (written by the reduce pass)
   act_t* sh_fwd;            // [k*k][Coutp][Cinp]
   act_t* sh_bwd;            // [k*k][Cinp][Coutp]
   // SEG_VEC: gradient = src_d[c*2 + comp] (double sums) for c < n
@@ -152,6 +153,9 @@ struct SgdSpec {
   float lr_np, momentum, wd, gamma;
   const int64_t* milestones; int n_ms; int64_t spe;
   const int64_t* n_p;       // device scalar: hybrid switch mini-batch (huge if none)
+  // split-K reduction pass (one launch for all conv segments, coalesced float4 over [rows][Coutp])
+  const int64_t* red_block_start;  // device: first reduce block of each segment (0 blocks for non-conv)
+  int64_t red_total_blocks;
 };
 void sgd_update(const SgdSpec& s, cudaStream_t st);
 // Writes the shadows from the master weights only (used at create / import).

@@ -78,7 +78,7 @@ int pst_op_conv2d_fwd(const float* x, const float* w, float* y, int N, int Cin, 
       const char* names[8] = {"prod_issue", "ev1", "ev2", "ev3", "ev4", "epi_start", "epi_done", "start"};
       for (int e = 0; e < 7; ++e) {
         std::printf("TL %-10s", names[e]);
-        for (int i = 0; i < 40 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (h[e * 256 + i] - h[7 * 256]) / 1e3);
+        for (int i = 0; i < 40 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (double)(long long)(h[e * 256 + i] - h[7 * 256]) / 1e3);
         std::printf("\n");
       }
     }
@@ -144,7 +144,7 @@ int pst_op_conv2d_wgrad(const float* x, const float* gy, float* gw, int N, int C
                               "epi_done", "start"};
       for (int e = 0; e < 6; ++e) {
         std::printf("TLW %-10s", names[e]);
-        for (int i = 0; i < 40 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (h[e * 256 + i] - h[7 * 256]) / 1e3);
+        for (int i = 0; i < 40 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (double)(long long)(h[e * 256 + i] - h[7 * 256]) / 1e3);
         std::printf("\n");
       }
     }
@@ -158,3 +158,73 @@ int pst_op_conv2d_wgrad(const float* x, const float* gy, float* gw, int N, int C
 // error text for ops calls: pst_last_error(NULL) returns the global message of pst_api.cu;
 // ops keep their own, exported for the binding.
 extern "C" const char* pst_op_last_error(void) { return g_err.c_str(); }
+
+// Kernel timing for tuning (tools/conv_lab.py): `which` 0 fwd, 1 dgrad, 2 wgrad of one
+// convolution shape on resident device buffers; warm-up, then `iters` launches timed with CUDA
+// events on one stream; *us = mean microseconds per launch.  Inputs are zero (MMA and TMA time
+// do not depend on values).
+extern "C" int pst_op_time_conv(int which, int N, int Cin, int H, int W, int Cout, int k, int stride, int pad,
+                                int iters, float* us) {
+  return run([&] {
+    Geo g = geo(N, Cin, H, W, Cout, k, stride, pad);
+    Scratch s;
+    cudaStream_t st;
+    PST_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    act_t* xa = s.get<act_t>((size_t)N * H * W * g.Cinp);
+    act_t* ya = s.get<act_t>((size_t)N * g.Ho * g.Wo * g.Coutp);
+    act_t* sf = s.get<act_t>((size_t)k * k * g.Coutp * g.Cinp * (PST_SPLIT ? 2 : 1));
+    double* stats = s.get<double>((size_t)2 * g.Coutp);
+    int dev;
+    PST_CUDA(cudaGetDevice(&dev));
+    WgradPlan p = wgrad_plan(N, H, W, g.Cinp, g.Ho, g.Wo, g.Coutp, k, stride, pad, num_sms(dev));
+    float* part = which == 2 ? s.get<float>((size_t)p.part_floats) : nullptr;
+    auto launch = [&] {
+      if (which == 0) {
+        ConvSpec c{};
+        c.in = xa; c.N = N; c.H = H; c.W = W; c.Cinp = g.Cinp;
+        c.Ho = g.Ho; c.Wo = g.Wo; c.Coutp = g.Coutp; c.Cout = Cout;
+        c.k = k; c.S = stride; c.off = -pad; c.sgn = 1;
+        c.wshadow = sf; c.epi = EPI_BN_STATS; c.out = ya; c.stats = stats;
+        conv_tc(c, st);
+      } else if (which == 1) {
+        PST_CHECK_ARG(stride == 1, "time dgrad: stride 1 only");
+        ConvSpec c{};
+        c.in = ya; c.N = N; c.H = g.Ho; c.W = g.Wo; c.Cinp = g.Coutp;
+        c.Ho = H; c.Wo = W; c.Coutp = g.Cinp; c.Cout = Cin;
+        c.k = k; c.S = 1; c.off = pad; c.sgn = -1;
+        c.wshadow = sf; c.epi = EPI_DGRAD; c.out = xa;
+        conv_tc(c, st);
+      } else {
+        WgradSpec wg{};
+        wg.x = xa; wg.N = N; wg.H = H; wg.W = W; wg.Cinp = g.Cinp;
+        wg.dy = ya; wg.Ho = g.Ho; wg.Wo = g.Wo; wg.Coutp = g.Coutp;
+        wg.k = k; wg.S = stride; wg.pad = pad; wg.part = part; wg.ksplit = p.ksplit;
+        conv_wgrad_tc(wg, st);
+      }
+    };
+    // the timed launches are one CUDA graph (as in the pipeline), so host launch cost is excluded
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    PST_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) launch();
+    PST_CUDA(cudaStreamEndCapture(st, &graph));
+    PST_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    PST_CUDA(cudaGraphLaunch(exec, st));
+    cudaEvent_t e0, e1;
+    PST_CUDA(cudaEventCreate(&e0));
+    PST_CUDA(cudaEventCreate(&e1));
+    PST_CUDA(cudaEventRecord(e0, st));
+    PST_CUDA(cudaGraphLaunch(exec, st));
+    PST_CUDA(cudaEventRecord(e1, st));
+    PST_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    PST_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *us = ms * 1e3f / (float)iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    PST_CUDA(cudaStreamSynchronize(st));
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(st);
+  });
+}

@@ -26,7 +26,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // Bounded wait: traps (instead of hanging the GPU) if the phase never completes.
+#ifndef PST_MBAR_OP
+#define PST_MBAR_OP "mbarrier.test_wait.parity.shared::cta.b64"
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        PST_MBAR_OP " p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (it > (1u << 30)) __trap();
+  }
+}
+
+// As mbar_wait, but backs off with nanosleep between polls (for warps that wait long).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
   uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
   for (uint32_t it = 0;; ++it) {
@@ -39,6 +59,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     if (done) return;
     if (it > (1u << 26)) __trap();
+    __nanosleep(ns);
   }
 }
 

@@ -2,9 +2,17 @@
 #include "stage.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace pst {
+
+// Timing experiments only (PST_SKIP=fwd,bnapply,bwdpre,bnbwd,wgrad,dgrad,sgd): leave a kernel class
+// out of the step to measure its in-graph cost.  Results are wrong when set.
+static bool skip(const char* cls) {
+  static const char* env = std::getenv("PST_SKIP");
+  return env != nullptr && std::strstr(env, cls) != nullptr;
+}
 
 template <typename T>
 T* Stage::alloc(size_t n, bool zero) {
@@ -106,11 +114,13 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
 
   // ---- optimiser segments
   std::vector<SgdSeg> segs;
-  std::vector<int64_t> starts;
-  int64_t blocks = 0;
+  std::vector<int64_t> starts, rstarts;
+  int64_t blocks = 0, rblocks = 0;
   auto add = [&](SgdSeg g) {
     starts.push_back(blocks);
+    rstarts.push_back(rblocks);
     blocks += (g.n + 255) / 256;
+    if (g.kind == SEG_CONVW) rblocks += ((int64_t)g.k * g.k * g.Cinp * g.Coutp / 4 + 255) / 256;
     segs.push_back(g);
   };
   for (int l = l0; l < l1; ++l) {
@@ -125,6 +135,7 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     g.Cinp = li.Cinp;
     g.part = b.wpart;
     g.ksplit = b.ksplit;
+    g.gsum = alloc<float>((size_t)li.kk * li.kk * li.Cinp * li.Coutp);
     g.sh_fwd = b.sh_fwd;
     g.sh_bwd = b.sh_bwd;
     g.kind = SEG_CONVW;   // FC over CxHxW = valid conv with k = H (canonical [o][c*H*W+y*W+x] == OIHW)
@@ -143,6 +154,9 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     }
   }
   starts.push_back(blocks);
+  rstarts.push_back(rblocks);
+  d_red_start_ = alloc<int64_t>(rstarts.size());
+  PST_CUDA(cudaMemcpy(d_red_start_, rstarts.data(), rstarts.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   d_segs_ = alloc<SgdSeg>(segs.size());
   PST_CUDA(cudaMemcpy(d_segs_, segs.data(), segs.size() * sizeof(SgdSeg), cudaMemcpyHostToDevice));
   d_seg_start_ = alloc<int64_t>(starts.size());
@@ -162,6 +176,8 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
   sgd_.n_segs = (int)segs.size();
   sgd_.seg_block_start = d_seg_start_;
   sgd_.total_blocks = blocks;
+  sgd_.red_block_start = d_red_start_;
+  sgd_.red_total_blocks = rblocks;
   sgd_.v_count = d_vcount_;
   sgd_.ticket = d_ticket_;
   sgd_.lr_pipe = d_lr_;
@@ -248,7 +264,7 @@ void Stage::enqueue_forward(int slot, cudaStream_t st) {
       c.epi = EPI_BIAS_ACT;
       c.out = b.z[slot];
     }
-    conv_tc(c, st);
+    if (!skip("fwd")) conv_tc(c, st);
     if (li.spec.bn) {
       BnApplySpec a{};
       a.y = b.y[slot]; a.z = b.z[slot];
@@ -268,7 +284,7 @@ void Stage::enqueue_forward(int slot, cudaStream_t st) {
         a.res_H = src.in_H; a.res_W = src.in_W; a.res_C = src.in_Cp; a.res_Creal = src.in_C;
         a.res_pad = li.res_pad;
       }
-      bn_apply(a, st);
+      if (!skip("bnapply")) bn_apply(a, st);
       ++bn_local;
     }
     if (li.spec.pool == PST_POOL_MAX2)
@@ -308,7 +324,7 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
     pr.gpre = b.gpre;
     pr.N = B; pr.H = li.Ho; pr.W = li.Wo; pr.Cp = li.Coutp; pr.C = li.spec.cout;
     pr.sums = b.sums;
-    bwd_pre(pr, st);
+    if (!skip("bwdpre")) bwd_pre(pr, st);
     const act_t* dY = b.gpre;
     if (li.spec.bn) {
       BnBwdSpec bb{};
@@ -316,7 +332,7 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
       bb.gamma = w_ + (li.off_g - p_base);  // current gamma (no stash)
       bb.gy = b.gy;
       bb.N = B; bb.H = li.Ho; bb.W = li.Wo; bb.Cp = li.Coutp; bb.C = li.spec.cout;
-      bn_bwd_apply(bb, st);
+      if (!skip("bnbwd")) bn_bwd_apply(bb, st);
       dY = b.gy;
     }
     // weight gradient from the saved input of this mini-batch
@@ -332,7 +348,7 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
     wg.pad = li.pad;
     wg.part = b.wpart;
     wg.ksplit = b.ksplit;
-    conv_wgrad_tc(wg, st);
+    if (!skip("wgrad")) conv_wgrad_tc(wg, st);
     // input gradient with the CURRENT weights
     if (b.gin != nullptr) {
       ConvSpec c{};
@@ -361,10 +377,10 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
         c.res_mode = e.res_mode;
         c.res_H = e.Ho; c.res_W = e.Wo; c.res_C = e.Coutp; c.res_pad = e.res_pad;
       }
-      conv_tc(c, st);
+      if (!skip("dgrad")) conv_tc(c, st);
     }
   }
-  sgd_update(sgd_, st);
+  if (!skip("sgd")) sgd_update(sgd_, st);
 }
 
 // ------------------------------------------------------------------ host readback

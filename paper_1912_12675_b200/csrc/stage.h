@@ -90,6 +90,7 @@ class Stage {
   // optimiser
   SgdSpec sgd_{};
   SgdSeg* d_segs_ = nullptr;
+  int64_t* d_red_start_ = nullptr;
   int64_t* d_seg_start_ = nullptr;
   int64_t* d_vcount_ = nullptr;
   int* d_ticket_ = nullptr;
