@@ -11,6 +11,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # PST_LIB=bf16 / f16 selects another precision build (libpst_bf16.so / libpst_f16.so)
 _LIB_PATH = os.path.join(_HERE, {"bf16": "libpst_bf16.so", "f16": "libpst_f16.so"}.get(
     os.environ.get("PST_LIB", ""), "libpst.so"))
+if os.environ.get("PST_LIB_PATH"):   # experiment builds (tools/); still the same C ABI
+    _LIB_PATH = os.environ["PST_LIB_PATH"]
 
 PST_OK = 0
 _STATUS = {0: "PST_OK", -1: "PST_E_INVALID", -2: "PST_E_OOM", -3: "PST_E_CUDA", -4: "PST_E_NCCL",

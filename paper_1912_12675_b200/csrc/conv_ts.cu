@@ -32,6 +32,7 @@ namespace {
 constexpr int kTsThreads = 448;   // warps: 0 TMA, 1 MMA, 2-5 epilogue, 6-13 converters
 constexpr int kMaxBand = 4;
 constexpr int kMaxSlots = 16;
+constexpr int kMaxAcc = 4;      // accumulator buffers (MMA runs up to kMaxAcc-1 tiles ahead of the epilogue)
 
 struct TsArgs {
   int N, Ho, Wo, Cinp, Coutp, Cout, BN, n_ntiles, n_mtiles, tpi;
@@ -41,6 +42,7 @@ struct TsArgs {
   int lo;                    // lowest tap offset (both dims)
   int band_stages, n_slots;
   int tps;                   // taps per TMEM A slot (one handshake)
+  int n_acc;                 // accumulator buffers in TMEM (2..kMaxAcc)
   int w3d;                   // weight tensor map form (3D long rows when BN*EPC <= 256)
   uint32_t band_bytes, band_tx, plane_bytes, w_bytes;
   int tapshift[49];          // band rows (16 B) between the tile origin and tap t's input
@@ -52,6 +54,8 @@ struct TsArgs {
   int res_mode, res_H, res_W, res_C, res_pad;
   unsigned long long* dbg;   // optional timeline (CTA 0), PST_DBG_TL
   int knob;                  // experiment switches (PST_TS_KNOB), 0 in production
+  const act_t* bz; const act_t* by; const float* bsaved; double* bsums;   // fused bwd_pre (EPI_DGRAD)
+  int bfuse, brelu, bbn;
 };
 
 __device__ __forceinline__ unsigned long long ts_gtime() {
@@ -68,7 +72,29 @@ __device__ __forceinline__ float ld_planar_f(const act_t* base, int64_t npix, in
   return act2f(base[((int64_t)(c / kEPC) * npix + pix) * kEPC + c % kEPC]);
 }
 
-template <int KC, int EPI>
+// Per-channel sums over a warp's 32 pixels of 16 channels (u, v per lane): reduce-scatter leaves
+// channel (lane >> 1) in lanes 2c, 2c+1; the even lane adds both sums into its fp64 slots w2.
+__device__ __forceinline__ void warp_chan_sums(float* s1, float* s2, int lane, double* w2) {
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1) {       // 16 -> 8 -> 4 -> 2 -> 1 values per lane
+    const bool up = (lane & (2 * w)) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float t1 = up ? s1[i] : s1[i + w], k1 = up ? s1[i + w] : s1[i];
+      const float t2 = up ? s2[i] : s2[i + w], k2 = up ? s2[i + w] : s2[i];
+      s1[i] = k1 + __shfl_xor_sync(0xffffffffu, t1, 2 * w);
+      s2[i] = k2 + __shfl_xor_sync(0xffffffffu, t2, 2 * w);
+    }
+  }
+  s1[0] += __shfl_xor_sync(0xffffffffu, s1[0], 1);
+  s2[0] += __shfl_xor_sync(0xffffffffu, s2[0], 1);
+  if ((lane & 1) == 0) {
+    w2[0] += (double)s1[0];
+    w2[1] += (double)s2[0];
+  }
+}
+
+template <int KC, int EPI, int TPS>
 __global__ void __launch_bounds__(kTsThreads, 1)
     conv_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, const TsArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -82,8 +108,8 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   uint64_t* afull = bempty + kMaxBand;
   uint64_t* aempty = afull + kMaxSlots;
   uint64_t* tfull = aempty + kMaxSlots;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* wbar = tempty + 2;
+  uint64_t* tempty = tfull + kMaxAcc;
+  uint64_t* wbar = tempty + kMaxAcc;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(wbar + 1);
   int* tsh = reinterpret_cast<int*>(tmem_ptr + 4);   // tap shifts (a.tapshift indexed dynamically
                                                      // from the param space would be copied to local memory)
@@ -98,7 +124,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.band_stages; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&bempty[i], 8); }
     for (int i = 0; i < a.n_slots; ++i) { ptx::mbar_init(&afull[i], 4); ptx::mbar_init(&aempty[i], 1); }
-    for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < a.n_acc; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 4); }
     ptx::mbar_init(wbar, 1);
     ptx::fence_mbar_init();
   }
@@ -116,7 +142,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   const uint32_t tmem = *tmem_ptr;
   pdl_wait();      // no global memory access above this line
   pdl_trigger();
-  const uint32_t a_col0 = 2 * a.BN;                  // accumulators: columns [0, 2 BN)
+  const uint32_t a_col0 = a.n_acc * a.BN;            // accumulators: columns [0, n_acc BN)
 
   if (a.knob & 16) {
     // experiment: prologue and teardown only
@@ -162,23 +188,26 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     ptx::mbar_wait(wbar, 0);
     int slot = 0;
     uint32_t sph = 0;
-    int local = 0;
-    const int ngrp = a.taps / a.tps;
-    for (int m = m0; m < a.n_mtiles; m += mstep, ++local) {
-      const int acc = local & 1;
-      ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
-      ptx::tc_fence_after();
+    int acc = 0;
+    uint32_t aph = 0;
+    const int ngrp = a.taps / TPS;
+    for (int m = m0; m < a.n_mtiles; m += mstep) {
+      ptx::mbar_wait(&tempty[acc], aph ^ 1);
+      if (!(a.knob & 256)) ptx::tc_fence_after();
       const uint32_t d = tmem + acc * a.BN;
       for (int kcc = 0; kcc < a.n_kc; ++kcc) {
         for (int gi = 0; gi < ngrp; ++gi) {
           ptx::mbar_wait(&afull[slot], sph);
-          ptx::tc_fence_after();
+          if (!(a.knob & 256)) ptx::tc_fence_after();
           if (lane == 0) TSL(4, dbg_i[4]++);
-          if (ptx::elect_one()) {
+          if (!(a.knob & 2) && ptx::elect_one()) {
             // one slot = tps taps x (KC hi + KC lo columns): 3 x KC/8 x tps MMAs per handshake
-            for (int i = 0; i < a.tps && !(a.knob & 2); ++i) {
-              const int t = gi * a.tps + i;
-              const uint32_t ahi = tmem + a_col0 + (slot * a.tps + i) * 2 * KC;
+            // compile-time trip counts: the elected lane's block is straight-line code (a runtime
+            // loop here costs an R2UR round trip per tcgen05.mma, ~4x the small-N MMA time)
+#pragma unroll
+            for (int i = 0; i < TPS; ++i) {
+              const int t = gi * TPS + i;
+              const uint32_t ahi = tmem + a_col0 + (slot * TPS + i) * 2 * KC;
               const uint64_t bt = ptx::desc_add(wdesc, t * wtap + kcc * (KC / kEPC) * (a.BN * 16));
 #pragma unroll
               for (int kk = 0; kk < KC / 8; ++kk) {
@@ -198,6 +227,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       }
       if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);
       __syncwarp();
+      if (++acc == a.n_acc) { acc = 0; aph ^= 1; }
     }
   } else if (warp >= 6) {
     // ---------------------------------------------------------------- converters (warps 6..13)
@@ -212,23 +242,27 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     const int per_img = a.rows_t * a.Wo;
     const int j = r / per_img, yy = (r / a.Wo) % a.rows_t, xx = r % a.Wo;
     const int pixoff = (j * a.Hb + yy * a.S) * a.Wb + xx * a.S;
-    const int ngrp = a.taps / a.tps;
+    const int ngrp = a.taps / TPS;
     int bs = 0;
     uint32_t bph = 0;
     uint32_t cnt = 0;                        // global group counter (same order as the MMA issuer)
+    int slot = 0;                            // slot / phase of group cnt (advanced for every group)
+    uint32_t sph = 0;
     for (int m = m0; m < a.n_mtiles; m += mstep) {
       for (int kcc = 0; kcc < a.n_kc; ++kcc) {
-        if (a.knob & 128) ptx::mbar_wait_sleep(&full[bs], bph, 100); else ptx::mbar_wait(&full[bs], bph);
+        ptx::mbar_wait(&full[bs], bph);
         const uint8_t* band = bands + bs * a.band_bytes;
-        for (int gi = (int)((cnt + set) & 1); gi < ngrp; gi += 2) {
-          const uint32_t c = cnt + gi;
-          const int slot = (int)(c % a.n_slots);
-          if (a.knob & 128) ptx::mbar_wait_sleep(&aempty[slot], ((c / a.n_slots) & 1) ^ 1, 100);
-          else ptx::mbar_wait(&aempty[slot], ((c / a.n_slots) & 1) ^ 1);
-          ptx::tc_fence_after();
+        for (int gi = 0; gi < ngrp; ++gi, ++cnt) {
+          const int my_slot = slot;
+          const uint32_t my_ph = sph;
+          if (++slot == a.n_slots) { slot = 0; sph ^= 1; }
+          if (((cnt ^ (uint32_t)set) & 1u) != 0) continue;   // the other set's group
+          ptx::mbar_wait(&aempty[my_slot], my_ph ^ 1);
+          if (!(a.knob & 256)) ptx::tc_fence_after();
           if (threadIdx.x == 192) TSL(1, dbg_i[1]++);
-          for (int i = 0; i < a.tps && !(a.knob & 1); ++i) {
-            const int t = gi * a.tps + i;
+#pragma unroll 1
+          for (int i = 0; i < TPS && !(a.knob & 1); ++i) {
+            const int t = gi * TPS + i;
             const uint8_t* src = band + (uint32_t)(pixoff + tsh[t]) * 16;
             float hi[KC], lo[KC];
 #pragma unroll
@@ -238,20 +272,19 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             }
 #pragma unroll
             for (int e = 0; e < KC; ++e) lo[e] = tf32_lo(hi[e]);
-            const uint32_t ta = tmem + lane_addr + a_col0 + (slot * a.tps + i) * 2 * KC;
+            const uint32_t ta = tmem + lane_addr + a_col0 + (my_slot * TPS + i) * 2 * KC;
 #pragma unroll
             for (int h = 0; h < KC / 16; ++h) {
               ptx::tmem_st16(ta + h * 16, hi + 16 * h);
               ptx::tmem_st16(ta + KC + h * 16, lo + 16 * h);
             }
           }
-          ptx::tmem_st_wait();
-          ptx::tc_fence_before();
+          if (!(a.knob & 512)) ptx::tmem_st_wait();
+          if (!(a.knob & 256)) ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&afull[slot]);
+          if (lane == 0) ptx::mbar_arrive(&afull[my_slot]);
           if (threadIdx.x == 192) TSL(3, dbg_i[3]++);
         }
-        cnt += ngrp;
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&bempty[bs]);
         if (++bs == a.band_stages) { bs = 0; bph ^= 1; }
@@ -268,22 +301,28 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     const int et = threadIdx.x - 64;         // 0..127
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     double* wacc = reinterpret_cast<double*>(sst);   // [4 warps][BN][2]  (<= 8 KB)
-    if (EPI == EPI_BN_STATS) {
+    const bool sums = EPI == EPI_BN_STATS || (EPI == EPI_DGRAD && a.bfuse);
+    if (sums) {
       for (int i = lane; i < 2 * a.BN; i += 32) wacc[q * 2 * a.BN + i] = 0.0;
       __syncwarp();
     }
     const int per_img = a.rows_t * a.Wo;
     const int64_t npix = (int64_t)a.N * a.Ho * a.Wo;
     const int ng = a.BN / 16;
-    int local = 0;
-    for (int m = m0; m < a.n_mtiles; m += mstep, ++local) {
-      const int acc = local & 1;
-      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
-      ptx::tc_fence_after();
+    // this thread's pixel inside a tile (fixed), and the tile origin advanced incrementally
+    const int jt = r / per_img, yt = (r / a.Wo) % a.rows_t, x = r % a.Wo;
+    int mq = a.nb > 1 ? m0 : m0 / a.tpi, mr = a.nb > 1 ? 0 : m0 % a.tpi;
+    const int sq = a.nb > 1 ? mstep : mstep / a.tpi, sr = a.nb > 1 ? 0 : mstep % a.tpi;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int m = m0; m < a.n_mtiles; m += mstep) {
+      ptx::mbar_wait(&tfull[acc], aph);
+      if (!(a.knob & 256)) ptx::tc_fence_after();
       if (threadIdx.x == 64) TSL(5, dbg_i[5]++);
-      const int n = (a.nb > 1 ? m * a.nb : m / a.tpi) + r / per_img;
-      const int y = (a.nb > 1 ? 0 : (m % a.tpi) * a.rows_t) + (r / a.Wo) % a.rows_t;
-      const int x = r % a.Wo;
+      const int n = (a.nb > 1 ? mq * a.nb : mq) + jt;
+      const int y = mr * a.rows_t + yt;
+      mq += sq; mr += sr;
+      if (mr >= a.tpi && a.nb == 1) { mr -= a.tpi; ++mq; }
       const bool valid = n < a.N;
       const int64_t pix = ((int64_t)n * a.Ho + y) * a.Wo + x;
       for (int g = 0; g < ng; ++g) {
@@ -293,9 +332,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           for (int i = 0; i < 16; ++i) u[i] = 0.f;
         } else ptx::tmem_ld16(tmem + lane_addr + acc * a.BN + g * 16, u);
         if (g == ng - 1) {
-          ptx::tc_fence_before();
+          if (!(a.knob & 256)) ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+          if (++acc == a.n_acc) { acc = 0; aph ^= 1; }
         }
         const int c0 = nt * a.BN + g * 16;
         if (EPI == EPI_BN_STATS) {
@@ -305,8 +345,12 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           }
         } else if (EPI == EPI_DGRAD) {   // + shortcut^T of the residual layer's gradient
           if (valid && a.res_mode == 1) {
+            const float* rs = reinterpret_cast<const float*>(a.res);   // act_t == float in this build
 #pragma unroll
-            for (int i = 0; i < 16; ++i) u[i] += ld_planar_f(a.res, npix, pix, c0 + i);
+            for (int jj = 0; jj < 4; ++jj) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(rs + ((int64_t)(c0 / 4 + jj) * npix + pix) * 4));
+              u[4 * jj] += v.x; u[4 * jj + 1] += v.y; u[4 * jj + 2] += v.z; u[4 * jj + 3] += v.w;
+            }
           } else if (valid && a.res_mode == 2 && ((y | x) & 1) == 0) {
             const int64_t rpix = ((int64_t)n * a.res_H + (y >> 1)) * a.res_W + (x >> 1);
             const int64_t rnpix = (int64_t)a.N * a.res_H * a.res_W;
@@ -314,6 +358,22 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             for (int i = 0; i < 16; ++i) {
               const int c = c0 + i;
               if (c < a.Cout) u[i] += ld_planar_f(a.res, rnpix, rpix, c + a.res_pad);
+            }
+          }
+          if (a.bfuse) {                   // fused bwd_pre: relu'(z) of the lower layer; zero padding pixels
+            if (!valid) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) u[i] = 0.f;
+            } else if (a.brelu) {
+              const float* zp = reinterpret_cast<const float*>(a.bz);
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const float4 zv = __ldg(reinterpret_cast<const float4*>(zp + ((int64_t)(c0 / 4 + jj) * npix + pix) * 4));
+                u[4 * jj] = zv.x > 0.f ? u[4 * jj] : 0.f;
+                u[4 * jj + 1] = zv.y > 0.f ? u[4 * jj + 1] : 0.f;
+                u[4 * jj + 2] = zv.z > 0.f ? u[4 * jj + 2] : 0.f;
+                u[4 * jj + 3] = zv.w > 0.f ? u[4 * jj + 3] : 0.f;
+              }
             }
           }
         } else {                           // EPI_BIAS_ACT / EPI_BIAS_F32
@@ -337,33 +397,40 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           float s1[16], s2[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) { s1[i] = u[i]; s2[i] = u[i] * u[i]; }
+          warp_chan_sums(s1, s2, lane, wacc + q * 2 * a.BN + 2 * (g * 16 + (lane >> 1)));
+        }
+        if (EPI == EPI_DGRAD && a.bfuse) {   // sums of the fused bwd_pre (u is the stored gpre)
+          float s1[16], s2[16];
+          if (a.bbn && valid) {
+            const float* yp = reinterpret_cast<const float*>(a.by);
 #pragma unroll
-          for (int w = 8; w >= 1; w >>= 1) {       // 16 -> 8 -> 4 -> 2 -> 1 values per lane
-            const bool up = (lane & (2 * w)) != 0;
+            for (int jj = 0; jj < 4; ++jj) {
+              const float4 yv = __ldg(reinterpret_cast<const float4*>(yp + ((int64_t)(c0 / 4 + jj) * npix + pix) * 4));
+              const float yy[4] = {yv.x, yv.y, yv.z, yv.w};
 #pragma unroll
-            for (int i = 0; i < w; ++i) {
-              const float t1 = up ? s1[i] : s1[i + w], k1 = up ? s1[i + w] : s1[i];
-              const float t2 = up ? s2[i] : s2[i + w], k2 = up ? s2[i + w] : s2[i];
-              s1[i] = k1 + __shfl_xor_sync(0xffffffffu, t1, 2 * w);
-              s2[i] = k2 + __shfl_xor_sync(0xffffffffu, t2, 2 * w);
+              for (int e = 0; e < 4; ++e) {
+                const int c = c0 + 4 * jj + e;
+                const float xh = (yy[e] - __ldg(&a.bsaved[2 * c])) * __ldg(&a.bsaved[2 * c + 1]);
+                s1[4 * jj + e] = u[4 * jj + e];
+                s2[4 * jj + e] = u[4 * jj + e] * xh;
+              }
             }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) { s1[i] = u[i]; s2[i] = 0.f; }
           }
-          s1[0] += __shfl_xor_sync(0xffffffffu, s1[0], 1);   // lanes 2c, 2c+1 hold channel c
-          s2[0] += __shfl_xor_sync(0xffffffffu, s2[0], 1);
-          if ((lane & 1) == 0) {
-            double* w2 = wacc + q * 2 * a.BN + 2 * (g * 16 + (lane >> 1));
-            w2[0] += (double)s1[0];
-            w2[1] += (double)s2[0];
-          }
+          warp_chan_sums(s1, s2, lane, wacc + q * 2 * a.BN + 2 * (g * 16 + (lane >> 1)));
         }
       }
       if (threadIdx.x == 64) TSL(6, dbg_i[6]++);
     }
-    if (EPI == EPI_BN_STATS) {
+    if (sums) {
+      double* dst = EPI == EPI_BN_STATS ? a.stats : a.bsums;
+      const int nreal = EPI == EPI_BN_STATS ? 2 * a.BN : 2 * min(a.BN, a.Cout - nt * a.BN);
       ptx::named_bar_sync(1, 128);
-      for (int i = et; i < 2 * a.BN; i += 128) {
+      for (int i = et; i < nreal; i += 128) {
         const double v = wacc[i] + wacc[2 * a.BN + i] + wacc[4 * a.BN + i] + wacc[6 * a.BN + i];
-        if (v != 0.0) atomicAdd(&a.stats[2 * nt * a.BN + i], v);
+        if (v != 0.0) atomicAdd(&dst[2 * nt * a.BN + i], v);
       }
     }
   }
@@ -410,15 +477,29 @@ static bool ts_plan(const ConvSpec& c, TsArgs& a, int& kc) {
   if (a.BN == 0) return false;
   a.n_ntiles = c.Coutp / a.BN;
   a.w_bytes = (uint32_t)a.taps * c.Cinp * a.BN * 4;
-  const int fixed = 2 * (int)a.w_bytes + 4 * 32 * 17 * 4 + 2048 + (2 * kMaxBand + 2 * kMaxSlots + 5) * 8 + 16 + 256;
+  const int fixed = 2 * (int)a.w_bytes + 4 * 32 * 17 * 4 + 2048 + (2 * kMaxBand + 2 * kMaxSlots + 2 * kMaxAcc + 1) * 8 + 16 + 256;
   a.band_stages = std::min(kMaxBand, (227 * 1024 - 1024 - fixed) / (int)a.band_bytes);
   if (a.band_stages < 2) return false;
-  a.tps = 1;
-  for (int tps : {3, 2, 1})
-    if (a.taps % tps == 0 && (512 - 2 * a.BN) / (2 * kc * tps) >= 2) { a.tps = tps; break; }
-  a.n_slots = std::min(kMaxSlots, (512 - 2 * a.BN) / (2 * kc * a.tps));
+  // accumulator buffers: as many as leave >= 3 A slots of the largest group (fall back to 2)
+  a.tps = 0;
+  a.n_acc = 0;
+  // (largest tap group first: every group costs one converter->MMA handshake)
+  for (int tps : {3, 2, 1}) {
+    if (a.taps % tps != 0) continue;
+    for (int nacc : {4, 3, 2})
+      if ((512 - nacc * a.BN) / (2 * kc * tps) >= (nacc > 2 ? 3 : 2)) { a.n_acc = nacc; break; }
+    if (a.n_acc) { a.tps = tps; break; }
+  }
+  if (a.tps == 0) return false;
+  a.n_slots = std::min(kMaxSlots, (512 - a.n_acc * a.BN) / (2 * kc * a.tps));
   if (a.n_slots < 2) return false;
   return true;
+}
+
+bool conv_ts_fits(const ConvSpec& c) {
+  TsArgs a;
+  int kc;
+  return ts_plan(c, a, kc);
 }
 
 bool conv_ts(const ConvSpec& c, cudaStream_t st) {
@@ -429,6 +510,8 @@ bool conv_ts(const ConvSpec& c, cudaStream_t st) {
   a.res = c.res; a.res_mode = c.res_mode; a.res_H = c.res_H; a.res_W = c.res_W; a.res_C = c.res_C;
   a.res_pad = c.res_pad;
   a.dbg = c.dbg;
+  a.bz = c.bz; a.by = c.by; a.bsaved = c.bsaved; a.bsums = c.bsums;
+  a.bfuse = c.bfuse; a.brelu = c.brelu; a.bbn = c.bbn;
   { static const char* kn = std::getenv("PST_TS_KNOB"); a.knob = kn ? std::atoi(kn) : 0; }
   // band box: (Wb*EPC, Hb, nb images, KC/EPC planes) of the planar input, zero outside
   uint64_t dims[4] = {(uint64_t)c.W * kEPC, (uint64_t)c.H, (uint64_t)c.N, (uint64_t)c.Cinp / kEPC};
@@ -450,12 +533,17 @@ bool conv_ts(const ConvSpec& c, cudaStream_t st) {
     tW = make_tmap(act_tmap_dtype(), 4, c.wshadow, wd, ws, wb, nullptr);
   }
   const size_t smem = 2 * (size_t)a.w_bytes + (size_t)a.band_stages * a.band_bytes + 4 * 32 * 17 * 4 + 2048 +
-                      (2 * kMaxBand + 2 * kMaxSlots + 5) * 8 + 16 + 256;
+                      (2 * kMaxBand + 2 * kMaxSlots + 2 * kMaxAcc + 1) * 8 + 16 + 256;
+  auto pick3 = [&](auto kcc, auto tpc) {
+    constexpr int K = decltype(kcc)::value, T = decltype(tpc)::value;
+    return c.epi == EPI_BN_STATS ? conv_ts_kernel<K, EPI_BN_STATS, T>
+         : c.epi == EPI_DGRAD    ? conv_ts_kernel<K, EPI_DGRAD, T>
+                                 : conv_ts_kernel<K, EPI_BIAS_ACT, T>;
+  };
   auto pick = [&](auto kcc) {
-    constexpr int K = decltype(kcc)::value;
-    return c.epi == EPI_BN_STATS ? conv_ts_kernel<K, EPI_BN_STATS>
-         : c.epi == EPI_DGRAD    ? conv_ts_kernel<K, EPI_DGRAD>
-                                 : conv_ts_kernel<K, EPI_BIAS_ACT>;
+    return a.tps == 3 ? pick3(kcc, std::integral_constant<int, 3>{})
+         : a.tps == 2 ? pick3(kcc, std::integral_constant<int, 2>{})
+                      : pick3(kcc, std::integral_constant<int, 1>{});
   };
   auto kern = kc == 32 ? pick(std::integral_constant<int, 32>{}) : pick(std::integral_constant<int, 16>{});
   PST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -478,6 +566,7 @@ bool conv_ts(const ConvSpec& c, cudaStream_t st) {
 }
 #else
 bool conv_ts(const ConvSpec&, cudaStream_t) { return false; }
+bool conv_ts_fits(const ConvSpec&) { return false; }
 #endif
 
 }  // namespace pst

@@ -40,8 +40,19 @@ struct WtArgs {
   int SB, St;                          // smem stages, TMEM A slots
   uint32_t rawx_bytes, rawx_tx, rawd_bytes, b_bytes, stage_bytes, sboB;
   float* part;
+  unsigned long long* dbg;   // optional timeline (CTA 0, clock64), PST_DBG_TL
 };
+#define WTL(ev, i)                                                                        \
+  do {                                                                                   \
+    if (a.dbg != nullptr && blockIdx.x == 0) {                                           \
+      const int i_ = (i);                                                                \
+      unsigned long long t_;                                                             \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));                                 \
+      if (i_ < 256) a.dbg[(ev) * 256 + i_] = t_;                                         \
+    }                                                                                    \
+  } while (0)
 
+template <int G, int P16>
 __global__ void __launch_bounds__(kWtThreads, 1)
     conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD,
                          const WtArgs a) {
@@ -57,6 +68,7 @@ __global__ void __launch_bounds__(kWtThreads, 1)
   uint64_t* tfull = afree + kWtMaxSlots;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(tfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) WTL(7, 0);
 
   const int b = blockIdx.x;
   const int mg = b % a.n_mgroups;
@@ -105,11 +117,14 @@ __global__ void __launch_bounds__(kWtThreads, 1)
       ptx::prefetch_tmap(&tmD);
     }
     __syncwarp();
+    int sb = 0;
+    uint32_t sbph = 0;
+    int uq = u_lo / a.ny, ur = u_lo % a.ny;   // unit -> (image group, row block), advanced incrementally
     for (int it = 0; it < n_iter; ++it) {
-      const int sb = it % a.SB;
-      const int u = u_lo + it;
-      const int n0 = (u / a.ny) * a.nb, y0 = (u % a.ny) * a.bh;
-      ptx::mbar_wait(&empty[sb], ((it / a.SB) & 1) ^ 1);
+      const int n0 = uq * a.nb, y0 = ur * a.bh;
+      if (++ur == a.ny) { ur = 0; ++uq; }
+      ptx::mbar_wait(&empty[sb], sbph ^ 1);
+      if (lane == 0) WTL(0, it);
       if (ptx::elect_one()) {
         uint8_t* s0 = ring + sb * a.stage_bytes;
         ptx::mbar_expect_tx(&full[sb], a.rawx_tx + a.rawd_bytes);
@@ -117,69 +132,88 @@ __global__ void __launch_bounds__(kWtThreads, 1)
         ptx::tma_load_4d(s0 + off_rawd, &tmD, &full[sb], 0, y0, n0, nt * (a.BNw / kEPC));
       }
       __syncwarp();
+      if (++sb == a.SB) { sb = 0; sbph ^= 1; }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     const uint32_t idesc = ptx::idesc_mma(128, a.BNw, 0, 0, 2);
+    int sb = 0, slot = 0;
+    uint32_t slph = 0;
     for (int it = 0; it < n_iter; ++it) {
-      const int sb = it % a.SB, slot = it % a.St;
-      ptx::mbar_wait(&ready[slot], (it / a.St) & 1);
+      ptx::mbar_wait(&ready[slot], slph);
       ptx::tc_fence_after();
+      if (lane == 0) WTL(4, it);
       const uint64_t bd0 = ptx::smem_desc(ptx::smem_u32(ring + sb * a.stage_bytes + off_b), 128, a.sboB);
       if (ptx::elect_one()) {
+        // straight-line block (compile-time G, P16): all G tiles are issued, a missing last
+        // tile only accumulates into an unused accumulator
         const uint32_t abase = tmem + acc_cols + slot * slot_cols;
-        for (int kk = 0; kk < a.P16 / 8; ++kk) {
+#pragma unroll
+        for (int kk = 0; kk < P16 / 8; ++kk) {
           const uint64_t bd = ptx::desc_add(bd0, kk * 256);
           const uint64_t bdl = ptx::desc_add(bd, a.b_bytes);
           const uint32_t acc0 = (it > 0 || kk > 0) ? 1u : 0u;
-          for (int j = 0; j < g_cnt; ++j) {
-            const uint32_t ahi = abase + j * 2 * a.P16 + kk * 8;
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            const uint32_t ahi = abase + j * 2 * P16 + kk * 8;
             const uint32_t d = tmem + j * a.BNw;
             ptx::umma_tf32_ts(d, ahi, bd, idesc, acc0);
             ptx::umma_tf32_ts(d, ahi, bdl, idesc, 1u);
-            ptx::umma_tf32_ts(d, ahi + a.P16, bd, idesc, 1u);
+            ptx::umma_tf32_ts(d, ahi + P16, bd, idesc, 1u);
           }
         }
         ptx::umma_commit(&empty[sb]);
         ptx::umma_commit(&afree[slot]);
       }
       __syncwarp();
+      if (lane == 0) WTL(2, it);
+      if (++sb == a.SB) sb = 0;
+      if (++slot == a.St) { slot = 0; slph ^= 1; }
     }
     if (n_iter > 0 && ptx::elect_one()) ptx::umma_commit(tfull);
     __syncwarp();
   } else {
     // ---------------------------------------------------------------- converters (warps 2..9)
+    // Two sets of 4 warps (one per TMEM lane quarter).  Set `set` converts pixel half `set`
+    // (16 of the unit's P16 <= 32 pixels) of every M tile the CTA owns, so both sets carry the
+    // same load; the band offsets of its 16 pixels are held in registers.
     const int q = warp & 3;
-    const int set = (warp - 2) >> 2;            // 0 or 1: M tiles j = set, set+2, ...
+    const int set = (warp - 2) >> 2;            // 0 or 1
     const int ct = threadIdx.x - 64;            // 0..255
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    // this thread's A rows (one per owned M tile): float offset of (tap, ci) in the band
-    int rb[4] = {-1, -1, -1, -1};
+    int rb[4] = {-1, -1, -1, -1};               // this thread's A row (one per owned M tile)
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int j = set + 2 * jj;
+    for (int j = 0; j < 4; ++j) {
       const int R = r0 + j * 128 + q * 32 + lane;
       if (j < g_cnt && R < r_end) {
         const int tap = R / a.Cinp, ci = R % a.Cinp;
         const int rr = tap / a.k, ss = tap % a.k;
         const int plane = ci / kEPC - pl0;
-        rb[jj] = ((plane * a.nb * a.band_r + rr) * a.band_c + ss) * 4 + ci % kEPC;
+        rb[j] = ((plane * a.nb * a.band_r + rr) * a.band_c + ss) * 4 + ci % kEPC;
       }
     }
+    const int p0 = set * 16;                    // this set's pixels [p0, p0 + 16) of the unit
+    int pb[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pb[i] = pixb[(p0 + i) & 127];
+    const bool has_px = p0 < a.P16;
     const int nq = a.P16 / 4;
     const int unitsB = (a.BNw / 4) * nq;
+    int sb = 0, slot = 0;
+    uint32_t sbph = 0, slph = 0;
     for (int it = 0; it < n_iter; ++it) {
-      const int sb = it % a.SB, slot = it % a.St;
-      ptx::mbar_wait(&full[sb], (it / a.SB) & 1);
-      ptx::mbar_wait(&afree[slot], ((it / a.St) & 1) ^ 1);
+      ptx::mbar_wait(&full[sb], sbph);
+      ptx::mbar_wait(&afree[slot], slph ^ 1);
       ptx::tc_fence_after();
+      if (threadIdx.x == 64) WTL(1, it);
       uint8_t* s0 = ring + sb * a.stage_bytes;
       const float* rawxf = reinterpret_cast<const float*>(s0);
       const float* rawdf = reinterpret_cast<const float*>(s0 + off_rawd);
       uint8_t* bhi = s0 + off_b;
       uint8_t* blo = bhi + a.b_bytes;
       // B: dY [co/4][P][4] -> K-major hi/lo rows (co) x pixels, 4 co x 4 px per task
-      for (int u = ct; u < unitsB; u += 256) {
+      // (spread over the 8 warps: task u runs on warp 2 + u % 8, lane 4 * ((u / 8) % 8))
+      for (int u = (lane % 4 == 0) ? (lane / 4) * 8 + (warp - 2) : unitsB; u < unitsB; u += 64) {
         const int kq = u % nq, cq = u / nq;
         float4 v[4];
 #pragma unroll
@@ -201,22 +235,20 @@ __global__ void __launch_bounds__(kWtThreads, 1)
           *reinterpret_cast<float4*>(blo + off) = make_float4(tf32_lo(h.x), tf32_lo(h.y), tf32_lo(h.z), tf32_lo(h.w));
         }
       }
-      // A: this thread's rows -> TMEM slot (hi columns [0,P16), lo columns [P16, 2 P16) per tile)
+      // A: rows -> TMEM slot (hi columns [0,P16), lo columns [P16, 2 P16) per tile), this set's pixels
+      if (has_px) {
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int j = set + 2 * jj;
-        if (j >= g_cnt) break;
-        const uint32_t ta = tmem + lane_addr + acc_cols + slot * slot_cols + j * 2 * a.P16;
-        for (int p0 = 0; p0 < a.P16; p0 += 16) {
+        for (int j = 0; j < 4; ++j) {
+          if (j >= g_cnt) break;
+          const uint32_t ta = tmem + lane_addr + acc_cols + slot * slot_cols + j * 2 * a.P16 + p0;
           float hv[16], lv[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const int pb = pixb[p0 + i];
-            hv[i] = (rb[jj] >= 0 && pb >= 0) ? rawxf[rb[jj] + pb] : 0.f;
+            hv[i] = (rb[j] >= 0 && pb[i] >= 0) ? rawxf[rb[j] + pb[i]] : 0.f;
             lv[i] = tf32_lo(hv[i]);
           }
-          ptx::tmem_st16(ta + p0, hv);
-          ptx::tmem_st16(ta + a.P16 + p0, lv);
+          ptx::tmem_st16(ta, hv);
+          ptx::tmem_st16(ta + a.P16, lv);
         }
       }
       ptx::tmem_st_wait();
@@ -224,6 +256,9 @@ __global__ void __launch_bounds__(kWtThreads, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&ready[slot]);
+      if (threadIdx.x == 64) WTL(3, it);
+      if (++sb == a.SB) { sb = 0; sbph ^= 1; }
+      if (++slot == a.St) { slot = 0; slph ^= 1; }
     }
     if (warp < 6) {
       // ---------------------------------------------------------------- epilogue (warps 2..5)
@@ -231,6 +266,7 @@ __global__ void __launch_bounds__(kWtThreads, 1)
         ptx::mbar_wait(tfull, 0);
         ptx::tc_fence_after();
       }
+      if (threadIdx.x == 64) WTL(5, 0);
       for (int j = 0; j < g_cnt; ++j) {
         const int R = r0 + j * 128 + q * 32 + lane;
         for (int ch = 0; ch < a.BNw / 16; ++ch) {
@@ -250,6 +286,7 @@ __global__ void __launch_bounds__(kWtThreads, 1)
       }
     }
   }
+  if (threadIdx.x == 64) WTL(6, 0);
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -282,7 +319,7 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   else { a.nb = std::max(1, std::min(N, ptarget / (Ho * Wo))); a.bh = Ho; }
   a.P = a.nb * a.bh * Wo;
   a.P16 = round_up(a.P, 16);
-  if (a.P16 > 128) return false;
+  if (a.P16 > 32) return false;   // two converter sets x 16 pixels
   a.band_r = (a.bh - 1) * S + k;
   a.band_c = (Wo - 1) * S + k;
   if (a.band_c * kEPC > 256 || a.band_r > 256) return false;
@@ -328,6 +365,7 @@ bool conv_wgrad_ts(const WgradSpec& w, cudaStream_t st) {
   if (!wgrad_ts_plan(w.N, w.H, w.W, w.Cinp, w.Ho, w.Wo, w.Coutp, w.k, w.S, w.pad, num_sms(dev), &a)) return false;
   PST_CHECK_ARG(a.ksplit == w.ksplit, "wgrad: workspace planned for a different split");
   a.part = w.part;
+  a.dbg = w.dbg;
   uint64_t xd[4] = {(uint64_t)w.W * kEPC, (uint64_t)w.H, (uint64_t)w.N, (uint64_t)w.Cinp / kEPC};
   uint64_t xs[3] = {(uint64_t)w.W * 16, (uint64_t)w.H * w.W * 16, (uint64_t)w.N * w.H * w.W * 16};
   uint32_t xb[4] = {(uint32_t)(a.band_c * kEPC), (uint32_t)a.band_r, (uint32_t)a.nb, (uint32_t)a.pl_grp};
@@ -338,14 +376,24 @@ bool conv_wgrad_ts(const WgradSpec& w, cudaStream_t st) {
   CUtensorMap tD = make_tmap(act_tmap_dtype(), 4, w.dy, dd, ds, db, nullptr);
   const size_t smem = (size_t)a.SB * a.stage_bytes + 128 * 4 + (2 * kWtMaxSB + 2 * kWtMaxSlots + 1) * 8 + 16;
   PST_CHECK_ARG(smem <= 227 * 1024, "wgrad smem budget");
-  PST_CUDA(cudaFuncSetAttribute(conv_wgrad_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  using KernT = void (*)(const CUtensorMap, const CUtensorMap, const WtArgs);
+  KernT kern = nullptr;
+  {
+    const KernT tab[2][4] = {{conv_wgrad_ts_kernel<1, 16>, conv_wgrad_ts_kernel<2, 16>, conv_wgrad_ts_kernel<3, 16>,
+                              conv_wgrad_ts_kernel<4, 16>},
+                             {conv_wgrad_ts_kernel<1, 32>, conv_wgrad_ts_kernel<2, 32>, conv_wgrad_ts_kernel<3, 32>,
+                              conv_wgrad_ts_kernel<4, 32>}};
+    PST_CHECK_ARG((a.P16 == 16 || a.P16 == 32) && a.G >= 1 && a.G <= 4, "wgrad tiling");
+    kern = tab[a.P16 == 32 ? 1 : 0][a.G - 1];
+  }
+  PST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = a.n_mgroups * a.n_ntiles * a.ksplit;
   const double es = sizeof(act_t);
   const double bytes = (double)w.N * w.H * w.W * w.Cinp * es + (double)w.N * w.Ho * w.Wo * w.Coutp * es +
                        (double)a.rows * w.Coutp * 4.0;   // algorithmic: X + dY read, dW written once
   const double flops = 2.0 * a.rows * (double)w.Coutp * w.N * w.Ho * w.Wo;
   prof::begin(st);
-  PST_CUDA(launch_k(conv_wgrad_ts_kernel, dim3(grid), dim3(kWtThreads), smem, st, tX, tD, a));
+  PST_CUDA(launch_k(kern, dim3(grid), dim3(kWtThreads), smem, st, tX, tD, a));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::CONV_WGRAD, bytes, flops);
   return true;

@@ -34,12 +34,18 @@ struct ConvSpec {
   const act_t* res;         // EPI_DGRAD residual gradient (identity or option A) or null
   int res_mode;             // 0 none, 1 identity, 2 option A
   int res_H, res_W, res_C, res_pad;
+  // EPI_DGRAD with bfuse: the output is the NEXT-lower layer's pre-activation gradient (the work
+  // of bwd_pre fused into the epilogue): gpre = relu'(bz) * (dgrad + res) is written to `out`,
+  // and sums[c] += (sum gpre, sum gpre * (by - mean) * invstd) with bsaved = (mean, invstd)
+  const act_t* bz; const act_t* by; const float* bsaved; double* bsums;
+  int bfuse, brelu, bbn;
   unsigned long long* dbg;  // optional device timeline buffer [8][256] (CTA 0), debug only
 };
 void conv_tc(const ConvSpec& c, cudaStream_t st);
 // TS-mode variant (A operand in tensor memory, 3xTF32 build); returns false if the shape
 // does not fit its tiling (conv_tc then runs the smem-operand kernel).
 bool conv_ts(const ConvSpec& c, cudaStream_t st);
+bool conv_ts_fits(const ConvSpec& c);   // conv_ts would take this shape
 
 // Weight gradient dW[tap*Cinp+ci][co] = sum_pixels X(shifted by tap)[p][ci] * dY[p][co],
 // split over pixel ranges: part[ks][rows][Coutp] float32 (reduced by sgd_update).

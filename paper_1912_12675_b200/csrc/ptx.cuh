@@ -27,7 +27,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 // Bounded wait: traps (instead of hanging the GPU) if the phase never completes.
 #ifndef PST_MBAR_OP
-#define PST_MBAR_OP "mbarrier.test_wait.parity.shared::cta.b64"
+#define PST_MBAR_OP "mbarrier.try_wait.parity.shared::cta.b64"   // HW sleep until phase / time limit
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
@@ -42,6 +42,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     if (done) return;
     if (it > (1u << 30)) __trap();
+#ifdef PST_MBAR_BACKOFF
+    __nanosleep(PST_MBAR_BACKOFF);
+#endif
   }
 }
 

@@ -4,11 +4,16 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 namespace pst {
 
 // Timing experiments only (PST_SKIP=fwd,bnapply,bwdpre,bnbwd,wgrad,dgrad,sgd): leave a kernel class
 // out of the step to measure its in-graph cost.  Results are wrong when set.
+static bool side_wgrad() {
+  static const bool on = [] { const char* e = std::getenv("PST_WSTREAM"); return e == nullptr || e[0] != '0'; }();
+  return on;
+}
 static bool skip(const char* cls) {
   static const char* env = std::getenv("PST_SKIP");
   return env != nullptr && std::strstr(env, cls) != nullptr;
@@ -30,6 +35,9 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     : s(s_), K(K_), l0(l0_), l1(l1_), dev(device), R(ring_slots(K_, s_)), batch_(batch), net_(net) {
   PST_CUDA(cudaSetDevice(dev));
   PST_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  PST_CUDA(cudaStreamCreateWithFlags(&wstream, cudaStreamNonBlocking));
+  PST_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  PST_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   const int B = batch;
   const int nsm = num_sms(dev);
   p_base = net.layers[l0].p_begin;
@@ -196,8 +204,12 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
 Stage::~Stage() {
   cudaSetDevice(dev);
   if (stream) cudaStreamSynchronize(stream);
+  if (wstream) cudaStreamSynchronize(wstream);
   for (void* p : allocs_) cudaFree(p);
   if (stream) cudaStreamDestroy(stream);
+  if (wstream) cudaStreamDestroy(wstream);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
 }
 
 void Stage::set_n_p(int64_t n_p) {
@@ -300,6 +312,8 @@ void Stage::enqueue_forward(int slot, cudaStream_t st) {
 // ------------------------------------------------------------------ backward + update
 void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
   const int B = batch_;
+  static const bool fuse_on = [] { const char* e = std::getenv("PST_FUSE_PRE"); return e == nullptr || e[0] != '0'; }();
+  std::vector<char> pre_done(l1 - l0, 0);   // bwd_pre(l) already done by dgrad(l+1)'s epilogue
   PST_CUDA(cudaMemsetAsync(bwd_arena_, 0, bwd_arena_n_ * sizeof(double), st));
   for (int l = l1 - 1; l >= l0; --l) {
     const LayerInfo& li = net_.layers[l];
@@ -324,7 +338,7 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
     pr.gpre = b.gpre;
     pr.N = B; pr.H = li.Ho; pr.W = li.Wo; pr.Cp = li.Coutp; pr.C = li.spec.cout;
     pr.sums = b.sums;
-    if (!skip("bwdpre")) bwd_pre(pr, st);
+    if (!skip("bwdpre") && !pre_done[l - l0]) bwd_pre(pr, st);
     const act_t* dY = b.gpre;
     if (li.spec.bn) {
       BnBwdSpec bb{};
@@ -348,7 +362,15 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
     wg.pad = li.pad;
     wg.part = b.wpart;
     wg.ksplit = b.ksplit;
-    if (!skip("wgrad")) conv_wgrad_tc(wg, st);
+    if (!skip("wgrad")) {
+      if (side_wgrad()) {
+        PST_CUDA(cudaEventRecord(ev_fork, st));
+        PST_CUDA(cudaStreamWaitEvent(wstream, ev_fork, 0));
+        conv_wgrad_tc(wg, wstream);
+      } else {
+        conv_wgrad_tc(wg, st);
+      }
+    }
     // input gradient with the CURRENT weights
     if (b.gin != nullptr) {
       ConvSpec c{};
@@ -371,6 +393,21 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
       c.wshadow = b.sh_bwd;
       c.epi = EPI_DGRAD;
       c.out = b.gin;
+      // fuse bwd_pre of layer l-1 (ReLU mask + BN backward sums) into this epilogue when layer
+      // l-1 has no pooling and the TS kernel takes the shape
+      if (fuse_on && l - 1 >= l0 && net_.layers[l - 1].spec.pool == 0 && conv_ts_fits(c)) {
+        const LayerInfo& lo = net_.layers[l - 1];
+        LayerBufs& bl = L_[l - 1 - l0];
+        c.out = bl.gpre;
+        c.bfuse = 1;
+        c.brelu = lo.spec.relu;
+        c.bbn = lo.spec.bn;
+        c.bz = bl.z.empty() ? nullptr : bl.z[slot];
+        c.by = lo.spec.bn ? bl.y[slot] : nullptr;
+        c.bsaved = lo.spec.bn ? bl.saved[slot] : nullptr;
+        c.bsums = bl.sums;
+        pre_done[l - 1 - l0] = 1;
+      }
       if (li.spec.block_begin && li.block_end >= 0) {
         const LayerInfo& e = net_.layers[li.block_end];
         c.res = L_[li.block_end - l0].gpre;
@@ -379,6 +416,10 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
       }
       if (!skip("dgrad")) conv_tc(c, st);
     }
+  }
+  if (side_wgrad()) {
+    PST_CUDA(cudaEventRecord(ev_join, wstream));
+    PST_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
   }
   if (!skip("sgd")) sgd_update(sgd_, st);
 }

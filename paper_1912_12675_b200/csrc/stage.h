@@ -62,6 +62,10 @@ class Stage {
   const int s, K, l0, l1, dev, R, batch_;
   int64_t p_base = 0, n_params = 0;
   cudaStream_t stream = nullptr;
+  // weight-gradient side stream: wgrad(l) depends only on dY(l) and the saved input, so it runs
+  // concurrently with the dgrad chain of the layers below and joins before the update
+  cudaStream_t wstream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool is_first() const { return s == 0; }
   bool is_last() const { return l1 == (int)net_.layers.size(); }
 

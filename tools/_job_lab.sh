@@ -1,2 +1,4 @@
-for k in 0 15; do LAB_TAG=knob$k PST_TS_KNOB=$k python tools/conv_lab.py 50 2>&1; done
-PST_TS_KNOB=15 python tools/tl_probe.py g1 fwd
+python tools/conv_lab.py 50 2>&1
+python tools/tl_probe.py g1 wgrad
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --profile-steps 0 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', round(d['ms_per_step'],3), round(d['value']))"
