@@ -18,6 +18,10 @@ def kernel_class(name):
         m = re.search(r"conv_fwd_kernel<([^>]*)>", name)
         dg = m and m.group(1).replace(" ", "").split(",")[-1] in ("true", "1", "(bool)1")
         return "conv_dgrad" if dg else "conv_fwd"
+    if "conv_ts_kernel" in name:   # template <KC, EPI, TPS>; EPI 3 = EPI_DGRAD
+        m = re.search(r"conv_ts_kernel<([^>]*)>", name)
+        epi = m.group(1).replace(" ", "").split(",")[1] if m else "0"
+        return "conv_dgrad" if epi == "3" else "conv_fwd"
     if "conv_wgrad" in name:
         return "conv_wgrad"
     for key, cls in (("bn_apply", "bn_apply"), ("bwd_pre", "bwd_pre"), ("bn_bwd", "bn_bwd"), ("maxpool", "pool"),
