@@ -133,20 +133,32 @@ def run_versioned(stages, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce, 
 
 
 def run_clocked(stages, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce, n_p=None,
-                snapshot=False):
-    """Oracle B: the step-clocked schedule with message passing and no weight history."""
+                snapshot=False, mom0=None):
+    """Oracle B: the step-clocked schedule with message passing and no weight history.
+
+    snapshot: False, True (per-stage params after every step, a list indexed by t), or a
+    container of step indices t (a dict {t: params} holding only those; for big nets).
+    mom0: initial momentum buffers per stage (default zero) -- lets a test restart the schedule
+    from a drained state (weights + momentum) taken from elsewhere."""
     K = len(stages)
     N = len(batches)
     n_pipe = N if n_p is None else min(n_p, N)
     W = [params0[s] for s in range(K)]
-    mom = [_zeros_like(params0[s]) for s in range(K)]
+    mom = [_zeros_like(params0[s]) for s in range(K)] if mom0 is None else [mom0[s] for s in range(K)]
     v = [0] * K
     ring = [dict() for _ in range(K)]
     inbox_f = [dict() for _ in range(K)]
     inbox_b = [dict() for _ in range(K)]
     dz = {}
     losses = [None] * N
-    log, snaps = [], []
+    log = []
+    snaps = [] if snapshot is True else {}
+
+    def keep(t):
+        if snapshot is True:
+            snaps.append([W[s] for s in range(K)])
+        elif snapshot and t in snapshot:
+            snaps[t] = [W[s] for s in range(K)]
 
     # ---- phase 1: pipelined steps (fill, steady state, drain of mbs < n_pipe)
     t = 0
@@ -179,8 +191,7 @@ def run_clocked(stages, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce, n_
             inbox_f[s][f] = a
         for (s, b, g) in out_b:
             inbox_b[s][b] = g
-        if snapshot:
-            snaps.append([W[s] for s in range(K)])
+        keep(t)
         t += 1
     assert all(len(r) == 0 for r in ring) and not dz
 
@@ -199,8 +210,7 @@ def run_clocked(stages, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce, n_
             g, G = stages[s].backward(W[s], caches[s], g)
             W[s], mom[s] = _sgd_stage(W[s], mom[s], G, learning_rate(hp, s, i, n_p), hp)
             v[s] += 1
-        if snapshot:
-            snaps.append([W[s] for s in range(K)])
+        keep(t)
         t += 1
     return Result(losses, W, mom, log, snaps if snapshot else None, stages=stages)
 

@@ -1084,14 +1084,26 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
       }
     }
   }
+  int nch_nh = nch;
   if (!halo) {
-    a.a_bytes = (uint32_t)nch * 2048;
-    a.b_bytes = (uint32_t)nch * a.BN * 16;
+    // the fixed smem (epilogue scratch, per-channel stat slots of all Coutp channels, barriers)
+    // grows with Coutp (e.g. AlexNet's FC 4096->2048 as a valid conv): shrink the channel chunk
+    // until two stages fit beside it
+    const int fixed = (16 * 129 + 4) * 4 + 2 * c.Coutp * 8 + (3 * kMaxStages + 5) * 8 + 16;
+    const int room = std::min(budget, 227 * 1024 - fixed);
+    for (int n = nch; n >= 2; n -= 2) {
+      if ((c.Cinp / kEPC) % n != 0) continue;
+      nch_nh = n;
+      if (2 * (n * 2048 + n * a.BN * 16) * xsplit <= room) break;
+    }
+    if (nch_nh != nch) { a.kc = nch_nh * kEPC; a.n_kc = c.Cinp / a.kc; }
+    a.a_bytes = (uint32_t)nch_nh * 2048;
+    a.b_bytes = (uint32_t)nch_nh * a.BN * 16;
     a.sb_bytes = a.b_bytes;
     a.wres_bytes = 0;
     a.tx_bytes = a.a_bytes + a.b_bytes * xsplit;
     a.stage_bytes = (a.a_bytes + a.b_bytes) * xsplit;
-    a.stages = std::max(2, std::min(kMaxStages, budget / (int)a.stage_bytes));
+    a.stages = std::max(2, std::min(kMaxStages, room / (int)a.stage_bytes));
   }
   a.tmem_cols = (uint32_t)std::max(32, pow2_at_least(2 * a.BN * (halo ? a.MT : 1)));
   a.epi = c.epi; a.relu = c.relu; a.out = c.out; a.bias = c.bias; a.stats = c.stats;
@@ -1109,10 +1121,10 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
     uint32_t box[4] = {(uint32_t)(a.Wv * kEPC), (uint32_t)band_r, 1, (uint32_t)nch_h};
     tA = make_tmap(act_tmap_dtype(), 4, c.in, dims, str, box, nullptr);
   } else {
-    tA = act_tmap(c.in, c.N, c.H, c.W, c.Cinp, a.bimg, a.bh, a.bw, c.S, nch);
+    tA = act_tmap(c.in, c.N, c.H, c.W, c.Cinp, a.bimg, a.bh, a.bw, c.S, nch_nh);
   }
   const int btaps = halo ? a.taps : 1;
-  const int nch_b = halo ? nch_h : nch;
+  const int nch_b = halo ? nch_h : nch_nh;
   CUtensorMap tB = w_tmap(c.wshadow, a.taps, c.Coutp, c.Cinp, a.BN, nch_b, btaps);
   CUtensorMap tBlo = PST_SPLIT ? w_tmap(c.wshadow + (size_t)a.taps * c.Coutp * c.Cinp, a.taps, c.Coutp, c.Cinp, a.BN,
                                         nch_b, btaps)

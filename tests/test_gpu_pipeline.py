@@ -14,7 +14,7 @@ import pytest
 torch = pytest.importorskip("torch")
 
 import pst_workloads as W
-from tests.parity import (L_TOL, W_TOL, flat_params, hparams, loss_errors, oracle_run, tensor_errors)
+from tests.parity import L_TOL, W_TOL, run_both
 
 pytestmark = pytest.mark.gpu
 
@@ -25,40 +25,6 @@ def pst():
         pytest.skip("no CUDA device")
     import paper_1912_12675_b200 as p
     return p
-
-
-def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, spe=1 << 62,
-             milestones=(), per_step=True, seed=5):
-    K = len(ppv) + 1
-    flat = W.init_params(net, seed=seed)
-    data = W.batches(net.in_shape, B, N, seed=seed + 100)
-    lr_np = lr[-1] if lr_np is None else lr_np
-    hp = hparams(lr, K, lr_np, mom, wd, milestones, 0.1, spe)
-    ref = oracle_run(net, flat, ppv, data, hp, n_p=n_p, snapshot=per_step)
-    pipe = pst.Pipeline(net, flat, ppv, B, lr, lr_np, momentum=mom, weight_decay=wd, milestones=milestones,
-                        steps_per_epoch=spe)
-    if n_p is not None:
-        assert n_p % spe == 0
-        pipe.set_hybrid(n_p // spe)
-    worst = (0.0, None)
-    t = 0
-    for i, (x, y) in enumerate(data):
-        pipe.step(x, y)
-        if per_step:
-            # a hybrid switch inserts the drain steps before this mini-batch's step
-            steps, _ = pipe.progress()
-            while t < steps - 1:
-                t += 1
-            e = tensor_errors(net, pipe.weights(), flat_params(net, ref.snapshots[steps - 1]))
-            worst = max(worst, e, key=lambda z: z[0])
-            t = steps
-    pipe.flush()
-    e = tensor_errors(net, pipe.weights(), flat_params(net, ref.params))
-    worst = max(worst, e, key=lambda z: z[0])
-    lerr = loss_errors(pipe.losses(0, N), ref.losses)
-    vers = pipe.versions()
-    pipe.close()
-    return worst, lerr, vers, ref
 
 
 @pytest.mark.parametrize("K,ppv", [(1, ()), (2, (3,)), (3, (1, 3))])
