@@ -200,7 +200,8 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           ptx::mbar_wait(&afull[slot], sph);
           if (!(a.knob & 256)) ptx::tc_fence_after();
           if (lane == 0) TSL(4, dbg_i[4]++);
-          if (!(a.knob & 2) && ptx::elect_one()) {
+          if (ptx::elect_one()) {
+            if (!(a.knob & 2)) {
             // one slot = tps taps x (KC hi + KC lo columns): 3 x KC/8 x tps MMAs per handshake
             // compile-time trip counts: the elected lane's block is straight-line code (a runtime
             // loop here costs an R2UR round trip per tcgen05.mma, ~4x the small-N MMA time)
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
                 ptx::umma_tf32_ts(d, ahi + kk * 8, bdl, idesc, 1u);
                 ptx::umma_tf32_ts(d, ahi + KC + kk * 8, bd, idesc, 1u);
               }
+            }
             }
             ptx::umma_commit(&aempty[slot]);
           }
