@@ -318,9 +318,6 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     int acc = 0;
     uint32_t aph = 0;
     for (int m = m0; m < a.n_mtiles; m += mstep) {
-      ptx::mbar_wait(&tfull[acc], aph);
-      if (!(a.knob & 256)) ptx::tc_fence_after();
-      if (threadIdx.x == 64) TSL(5, dbg_i[5]++);
       const int n = (a.nb > 1 ? mq * a.nb : mq) + jt;
       const int y = mr * a.rows_t + yt;
       mq += sq; mr += sr;
@@ -328,6 +325,29 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       const bool valid = n < a.N;
       const int64_t pix = ((int64_t)n * a.Ho + y) * a.Wo + x;
       for (int g = 0; g < ng; ++g) {
+        // dgrad: the group's global operands (residual gradient, the lower layer's z and y) are
+        // loaded first -- for g == 0 before waiting for the accumulator -- so their latency
+        // overlaps the MMAs instead of stalling the epilogue three times per group
+        float4 rv[4], zv[4], yv[4];
+        if (EPI == EPI_DGRAD) {
+          const int cq0 = (nt * a.BN + g * 16) / 4;
+          const bool r1 = valid && a.res_mode == 1;
+          const bool zr = valid && a.bfuse && a.brelu;
+          const bool yb = valid && a.bfuse && a.bbn;
+          const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int64_t off = ((int64_t)(cq0 + jj) * npix + pix) * 4;
+            rv[jj] = r1 ? __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.res) + off)) : z4;
+            zv[jj] = zr ? __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.bz) + off)) : z4;
+            yv[jj] = yb ? __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.by) + off)) : z4;
+          }
+        }
+        if (g == 0) {
+          ptx::mbar_wait(&tfull[acc], aph);
+          if (!(a.knob & 256)) ptx::tc_fence_after();
+          if (threadIdx.x == 64) TSL(5, dbg_i[5]++);
+        }
         float u[16];
         if (a.knob & 64) {
 #pragma unroll
@@ -346,11 +366,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             for (int i = 0; i < 16; ++i) u[i] = 0.f;
           }
         } else if (EPI == EPI_DGRAD) {   // + shortcut^T of the residual layer's gradient
-          if (valid && a.res_mode == 1) {
-            const float* rs = reinterpret_cast<const float*>(a.res);   // act_t == float in this build
+          if (valid && a.res_mode == 1) {   // act_t == float in this build
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-              const float4 v = __ldg(reinterpret_cast<const float4*>(rs + ((int64_t)(c0 / 4 + jj) * npix + pix) * 4));
+              const float4 v = rv[jj];
               u[4 * jj] += v.x; u[4 * jj + 1] += v.y; u[4 * jj + 2] += v.z; u[4 * jj + 3] += v.w;
             }
           } else if (valid && a.res_mode == 2 && ((y | x) & 1) == 0) {
@@ -367,14 +386,12 @@ __global__ void __launch_bounds__(kTsThreads, 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) u[i] = 0.f;
             } else if (a.brelu) {
-              const float* zp = reinterpret_cast<const float*>(a.bz);
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj) {
-                const float4 zv = __ldg(reinterpret_cast<const float4*>(zp + ((int64_t)(c0 / 4 + jj) * npix + pix) * 4));
-                u[4 * jj] = zv.x > 0.f ? u[4 * jj] : 0.f;
-                u[4 * jj + 1] = zv.y > 0.f ? u[4 * jj + 1] : 0.f;
-                u[4 * jj + 2] = zv.z > 0.f ? u[4 * jj + 2] : 0.f;
-                u[4 * jj + 3] = zv.w > 0.f ? u[4 * jj + 3] : 0.f;
+                u[4 * jj] = zv[jj].x > 0.f ? u[4 * jj] : 0.f;
+                u[4 * jj + 1] = zv[jj].y > 0.f ? u[4 * jj + 1] : 0.f;
+                u[4 * jj + 2] = zv[jj].z > 0.f ? u[4 * jj + 2] : 0.f;
+                u[4 * jj + 3] = zv[jj].w > 0.f ? u[4 * jj + 3] : 0.f;
               }
             }
           }
@@ -404,11 +421,9 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         if (EPI == EPI_DGRAD && a.bfuse) {   // sums of the fused bwd_pre (u is the stored gpre)
           float s1[16], s2[16];
           if (a.bbn && valid) {
-            const float* yp = reinterpret_cast<const float*>(a.by);
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-              const float4 yv = __ldg(reinterpret_cast<const float4*>(yp + ((int64_t)(c0 / 4 + jj) * npix + pix) * 4));
-              const float yy[4] = {yv.x, yv.y, yv.z, yv.w};
+              const float yy[4] = {yv[jj].x, yv[jj].y, yv[jj].z, yv[jj].w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const int c = c0 + 4 * jj + e;

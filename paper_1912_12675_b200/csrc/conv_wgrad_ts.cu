@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kWtThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.SB; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
-    for (int i = 0; i < a.St; ++i) { ptx::mbar_init(&ready[i], 8); ptx::mbar_init(&afree[i], 1); }
+    for (int i = 0; i < a.St; ++i) { ptx::mbar_init(&ready[i], 4); ptx::mbar_init(&afree[i], 1); }
     ptx::mbar_init(tfull, 1);
     ptx::fence_mbar_init();
   }
@@ -174,12 +174,12 @@ __global__ void __launch_bounds__(kWtThreads, 1)
     __syncwarp();
   } else {
     // ---------------------------------------------------------------- converters (warps 2..9)
-    // Two sets of 4 warps (one per TMEM lane quarter).  Set `set` converts pixel half `set`
-    // (16 of the unit's P16 <= 32 pixels) of every M tile the CTA owns, so both sets carry the
-    // same load; the band offsets of its 16 pixels are held in registers.
+    // Two sets of 4 warps (one warp per TMEM lane quarter each) take alternate iterations, so two
+    // units are converted concurrently (the per-unit chain -- shared loads, hi/lo split,
+    // tcgen05.st, wait::st -- is latency-bound).  A set converts all P16 pixels of its unit for
+    // every M tile the CTA owns, and the unit's dY block into the K-major hi/lo B rows.
     const int q = warp & 3;
     const int set = (warp - 2) >> 2;            // 0 or 1
-    const int ct = threadIdx.x - 64;            // 0..255
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     int rb[4] = {-1, -1, -1, -1};               // this thread's A row (one per owned M tile)
 #pragma unroll
@@ -192,28 +192,28 @@ __global__ void __launch_bounds__(kWtThreads, 1)
         rb[j] = ((plane * a.nb * a.band_r + rr) * a.band_c + ss) * 4 + ci % kEPC;
       }
     }
-    const int p0 = set * 16;                    // this set's pixels [p0, p0 + 16) of the unit
-    int pb[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) pb[i] = pixb[(p0 + i) & 127];
-    const bool has_px = p0 < a.P16;
     const int nq = a.P16 / 4;
     const int unitsB = (a.BNw / 4) * nq;
     int sb = 0, slot = 0;
     uint32_t sbph = 0, slph = 0;
     for (int it = 0; it < n_iter; ++it) {
-      ptx::mbar_wait(&full[sb], sbph);
-      ptx::mbar_wait(&afree[slot], slph ^ 1);
+      const int my_sb = sb, my_slot = slot;
+      const uint32_t my_sbph = sbph, my_slph = slph;
+      if (++sb == a.SB) { sb = 0; sbph ^= 1; }
+      if (++slot == a.St) { slot = 0; slph ^= 1; }
+      if ((it & 1) != set) continue;             // the other set's unit
+      ptx::mbar_wait(&full[my_sb], my_sbph);
+      ptx::mbar_wait(&afree[my_slot], my_slph ^ 1);
       ptx::tc_fence_after();
       if (threadIdx.x == 64) WTL(1, it);
-      uint8_t* s0 = ring + sb * a.stage_bytes;
+      uint8_t* s0 = ring + my_sb * a.stage_bytes;
       const float* rawxf = reinterpret_cast<const float*>(s0);
       const float* rawdf = reinterpret_cast<const float*>(s0 + off_rawd);
       uint8_t* bhi = s0 + off_b;
       uint8_t* blo = bhi + a.b_bytes;
       // B: dY [co/4][P][4] -> K-major hi/lo rows (co) x pixels, 4 co x 4 px per task
-      // (spread over the 8 warps: task u runs on warp 2 + u % 8, lane 4 * ((u / 8) % 8))
-      for (int u = (lane % 4 == 0) ? (lane / 4) * 8 + (warp - 2) : unitsB; u < unitsB; u += 64) {
+      // (the set's even lanes: task u runs on warp quarter u % 4, lane 2 * ((u / 4) % 16))
+      for (int u = (lane % 2 == 0) ? (lane / 2) * 4 + q : unitsB; u < unitsB; u += 64) {
         const int kq = u % nq, cq = u / nq;
         float4 v[4];
 #pragma unroll
@@ -235,30 +235,30 @@ __global__ void __launch_bounds__(kWtThreads, 1)
           *reinterpret_cast<float4*>(blo + off) = make_float4(tf32_lo(h.x), tf32_lo(h.y), tf32_lo(h.z), tf32_lo(h.w));
         }
       }
-      // A: rows -> TMEM slot (hi columns [0,P16), lo columns [P16, 2 P16) per tile), this set's pixels
-      if (has_px) {
+      // A: rows -> TMEM slot (hi columns [0,P16), lo columns [P16, 2 P16) per tile), all pixels
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (j >= g_cnt) break;
-          const uint32_t ta = tmem + lane_addr + acc_cols + slot * slot_cols + j * 2 * a.P16 + p0;
+      for (int j = 0; j < 4; ++j) {
+        if (j >= g_cnt) break;
+        const uint32_t ta = tmem + lane_addr + acc_cols + my_slot * slot_cols + j * 2 * a.P16;
+#pragma unroll
+        for (int h = 0; h < P16 / 16; ++h) {
           float hv[16], lv[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            hv[i] = (rb[j] >= 0 && pb[i] >= 0) ? rawxf[rb[j] + pb[i]] : 0.f;
+            const int pbv = pixb[h * 16 + i];       // broadcast shared load
+            hv[i] = (rb[j] >= 0 && pbv >= 0) ? rawxf[rb[j] + pbv] : 0.f;
             lv[i] = tf32_lo(hv[i]);
           }
-          ptx::tmem_st16(ta, hv);
-          ptx::tmem_st16(ta + a.P16, lv);
+          ptx::tmem_st16(ta + h * 16, hv);
+          ptx::tmem_st16(ta + a.P16 + h * 16, lv);
         }
       }
       ptx::tmem_st_wait();
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&ready[slot]);
+      if (lane == 0) ptx::mbar_arrive(&ready[my_slot]);
       if (threadIdx.x == 64) WTL(3, it);
-      if (++sb == a.SB) { sb = 0; sbph ^= 1; }
-      if (++slot == a.St) { slot = 0; slph ^= 1; }
     }
     if (warp < 6) {
       // ---------------------------------------------------------------- epilogue (warps 2..5)
