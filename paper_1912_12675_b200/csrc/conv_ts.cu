@@ -29,7 +29,11 @@ namespace pst {
 #if PST_SPLIT
 namespace {
 
-constexpr int kTsThreads = 448;   // warps: 0 TMA, 1 MMA, 2-5 epilogue, 6-13 converters
+#ifndef PST_TS_SETS
+#define PST_TS_SETS 2
+#endif
+constexpr int kTsSets = PST_TS_SETS;               // converter sets (4 warps each) taking groups in turn
+constexpr int kTsThreads = (6 + 4 * kTsSets) * 32;  // warps: 0 TMA, 1 MMA, 2-5 epilogue, 6.. converters
 constexpr int kMaxBand = 4;
 constexpr int kMaxSlots = 16;
 constexpr int kMaxAcc = 4;      // accumulator buffers (MMA runs up to kMaxAcc-1 tiles ahead of the epilogue)
@@ -122,7 +126,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   const int planes_w = a.Cinp / kEPC;                // weight planes per tap
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < a.band_stages; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&bempty[i], 8); }
+    for (int i = 0; i < a.band_stages; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&bempty[i], 4 * kTsSets); }
     for (int i = 0; i < a.n_slots; ++i) { ptx::mbar_init(&afull[i], 4); ptx::mbar_init(&aempty[i], 1); }
     for (int i = 0; i < a.n_acc; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 4); }
     ptx::mbar_init(wbar, 1);
@@ -232,9 +236,9 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       if (++acc == a.n_acc) { acc = 0; aph ^= 1; }
     }
   } else if (warp >= 6) {
-    // ---------------------------------------------------------------- converters (warps 6..13)
-    // Two sets of 4 warps (one warp per TMEM lane quarter each) take alternate tap groups of
-    // the global sequence.  Per group: for each of its tps taps, load the pixel's shifted input
+    // ---------------------------------------------------------------- converters (warps 6..)
+    // kTsSets sets of 4 warps (one warp per TMEM lane quarter each) take the tap groups of the
+    // global sequence in turn (several groups in flight hide the tcgen05.st -> wait::st latency).  Per group: for each of its tps taps, load the pixel's shifted input
     // channels from the band, split hi/lo, tcgen05.st both (no wait); one wait + one arrive
     // per group, so loads and stores of consecutive taps overlap.
     const int q = warp & 3;                  // TMEM lane quarter of this warp
@@ -247,18 +251,20 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     const int ngrp = a.taps / TPS;
     int bs = 0;
     uint32_t bph = 0;
-    uint32_t cnt = 0;                        // global group counter (same order as the MMA issuer)
+    int turn = 0;                            // set owning the next group (same order as the MMA issuer)
     int slot = 0;                            // slot / phase of group cnt (advanced for every group)
     uint32_t sph = 0;
     for (int m = m0; m < a.n_mtiles; m += mstep) {
       for (int kcc = 0; kcc < a.n_kc; ++kcc) {
         ptx::mbar_wait(&full[bs], bph);
         const uint8_t* band = bands + bs * a.band_bytes;
-        for (int gi = 0; gi < ngrp; ++gi, ++cnt) {
+        for (int gi = 0; gi < ngrp; ++gi) {
           const int my_slot = slot;
           const uint32_t my_ph = sph;
           if (++slot == a.n_slots) { slot = 0; sph ^= 1; }
-          if (((cnt ^ (uint32_t)set) & 1u) != 0) continue;   // the other set's group
+          const bool mine = turn == set;
+          if (++turn == kTsSets) turn = 0;
+          if (!mine) continue;                               // another set's group
           ptx::mbar_wait(&aempty[my_slot], my_ph ^ 1);
           if (!(a.knob & 256)) ptx::tc_fence_after();
           if (threadIdx.x == 192) TSL(1, dbg_i[1]++);
@@ -487,10 +493,14 @@ static bool ts_plan(const ConvSpec& c, TsArgs& a, int& kc) {
   a.plane_bytes = (uint32_t)a.nb * a.Hb * a.Wb * 16;
   a.band_tx = a.plane_bytes * (kc / kEPC);
   a.band_bytes = (uint32_t)round_up((int)a.band_tx, 1024);
-  // N tile: resident hi+lo weights of all taps <= 112 KB
+  // N tile: resident hi+lo weights of all taps <= wmax KB (PST_TS_WMAX: planning experiments;
+  // 150 lets the 64-channel convs take BN = 32: half the N tiles, each MMA twice as wide)
+  static const int wmax = [] { const char* e = std::getenv("PST_TS_WMAX"); return e ? std::atoi(e) : 150; }();
+  static const int force_tps = [] { const char* e = std::getenv("PST_TS_TPS"); return e ? std::atoi(e) : 0; }();
+  static const int force_nacc = [] { const char* e = std::getenv("PST_TS_NACC"); return e ? std::atoi(e) : 0; }();
   a.BN = 0;
   for (int bn = std::min(c.Coutp, 128); bn >= 16; bn -= 16)
-    if (c.Coutp % bn == 0 && 2ll * a.taps * c.Cinp * bn * 4 <= 112 * 1024) { a.BN = bn; break; }
+    if (c.Coutp % bn == 0 && 2ll * a.taps * c.Cinp * bn * 4 <= (int64_t)wmax * 1024) { a.BN = bn; break; }
   if (a.BN == 0) return false;
   a.n_ntiles = c.Coutp / a.BN;
   a.w_bytes = (uint32_t)a.taps * c.Cinp * a.BN * 4;
@@ -502,14 +512,18 @@ static bool ts_plan(const ConvSpec& c, TsArgs& a, int& kc) {
   a.n_acc = 0;
   // (largest tap group first: every group costs one converter->MMA handshake)
   for (int tps : {3, 2, 1}) {
-    if (a.taps % tps != 0) continue;
-    for (int nacc : {4, 3, 2})
-      if ((512 - nacc * a.BN) / (2 * kc * tps) >= (nacc > 2 ? 3 : 2)) { a.n_acc = nacc; break; }
+    if (a.taps % tps != 0 || (force_tps && tps != force_tps)) continue;
+    for (int nacc : {4, 3, 2}) {
+      if (force_nacc && nacc != force_nacc) continue;
+      // a set may reuse a slot only after the group kTsSets earlier completed its own wait on it
+      // (mbarrier parity aliasing): n_slots >= kTsSets
+      if ((512 - nacc * a.BN) / (2 * kc * tps) >= std::max(nacc > 2 ? 3 : 2, kTsSets)) { a.n_acc = nacc; break; }
+    }
     if (a.n_acc) { a.tps = tps; break; }
   }
   if (a.tps == 0) return false;
   a.n_slots = std::min(kMaxSlots, (512 - a.n_acc * a.BN) / (2 * kc * a.tps));
-  if (a.n_slots < 2) return false;
+  if (a.n_slots < std::max(2, kTsSets)) return false;
   return true;
 }
 

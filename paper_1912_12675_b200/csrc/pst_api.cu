@@ -382,6 +382,24 @@ int pst_create(const pst_net* net, const pst_partition* part, const pst_hparams*
       std::memcpy(&id, dist->nccl_id, sizeof(id));
       PST_CUDA(cudaSetDevice(c->devices[c->rank]));
       PST_NCCL(ncclCommInitRank(&c->comm, c->K, id, c->rank));
+      // Establish the P2P connections to both neighbours eagerly (one small exchange outside any
+      // stream capture): NCCL connects lazily on first use, and the step graphs capture the
+      // exchange, so the first captured send/recv must find the connection already set up.
+      Stage* S = c->stages[0].get();
+      void* wbuf = nullptr;
+      PST_CUDA(cudaMalloc(&wbuf, 2 * 256));
+      PST_CUDA(cudaMemset(wbuf, 0, 2 * 256));
+      const int s = c->rank;
+      for (int pass = 0; pass < 2; ++pass) {   // fwd direction, then bwd direction
+        PST_NCCL(ncclGroupStart());
+        if (pass == 0 && s < c->K - 1) PST_NCCL(ncclSend(wbuf, 256, ncclUint8, s + 1, c->comm, S->stream));
+        if (pass == 0 && s > 0) PST_NCCL(ncclRecv((char*)wbuf + 256, 256, ncclUint8, s - 1, c->comm, S->stream));
+        if (pass == 1 && s > 0) PST_NCCL(ncclSend(wbuf, 256, ncclUint8, s - 1, c->comm, S->stream));
+        if (pass == 1 && s < c->K - 1) PST_NCCL(ncclRecv((char*)wbuf + 256, 256, ncclUint8, s + 1, c->comm, S->stream));
+        PST_NCCL(ncclGroupEnd());
+      }
+      PST_CUDA(cudaStreamSynchronize(S->stream));
+      PST_CUDA(cudaFree(wbuf));
     }
     const size_t xb = (size_t)c->batch * c->net.in_C * c->net.in_H * c->net.in_W;
     for (int i = 0; i < 2; ++i) {

@@ -61,3 +61,26 @@ def test_hybrid_switch(pst):
     assert worst[0] <= W_TOL, worst
     assert lerr <= L_TOL, lerr
     assert list(vers) == [9, 9, 9]
+
+
+def test_distributed_mode_single_rank(pst):
+    """The one-process-per-GPU code path (pst_dist: ncclCommInitRank, the eager neighbour
+    warm-up, the per-rank step program) with world size 1 on cuda:0: it must train exactly like
+    local mode and the oracle (more ranks need more GPUs than this box has; the message pattern
+    of K > 1 is checked over gloo in test_dist_gloo.py)."""
+    import numpy as np
+    from oracle import network as Net
+    from tests.parity import hparams, oracle_run, flat_params, tensor_errors, loss_errors
+    net = W.tiny_resnet(width=16, hw=8, n=1)
+    flat = W.init_params(net, seed=11)
+    data = W.batches(net.in_shape, 32, 6, seed=12)
+    ref = oracle_run(net, flat, (), data, hparams([0.05], 1, 0.05, 0.9, 1e-4))
+    pipe = pst.Pipeline(net, flat, (), 32, [0.05], 0.05, momentum=0.9, weight_decay=1e-4, devices=[0], rank=0,
+                        nccl_id=pst.nccl_unique_id())
+    for x, y in data:
+        pipe.step(x, y)
+    pipe.flush()
+    e = tensor_errors(net, pipe.weights(), flat_params(net, ref.params))
+    assert e[0] <= W_TOL, e
+    assert loss_errors(pipe.losses(0, 6), ref.losses) <= L_TOL
+    pipe.close()
