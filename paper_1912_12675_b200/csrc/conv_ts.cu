@@ -48,6 +48,9 @@ struct TsArgs {
   int tps;                   // taps per TMEM A slot (one handshake)
   int n_acc;                 // accumulator buffers in TMEM (2..kMaxAcc)
   int w3d;                   // weight tensor map form (3D long rows when BN*EPC <= 256)
+  int stack;                 // N-stacked weights: per plane [hi rows | lo rows], one N = 2 BN MMA
+                             // computes A_hi*W_hi and A_hi*W_lo, a second (N = BN) A_lo*W_hi
+  int accw;                  // TMEM columns per accumulator buffer (2 BN stacked, else BN)
   uint32_t band_bytes, band_tx, plane_bytes, w_bytes;
   int tapshift[49];          // band rows (16 B) between the tile origin and tap t's input
   int epi, relu;
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   const uint32_t tmem = *tmem_ptr;
   pdl_wait();      // no global memory access above this line
   pdl_trigger();
-  const uint32_t a_col0 = a.n_acc * a.BN;            // accumulators: columns [0, n_acc BN)
+  const uint32_t a_col0 = a.n_acc * a.accw;          // accumulators: columns [0, n_acc accw)
 
   if (a.knob & 16) {
     // experiment: prologue and teardown only
@@ -156,7 +159,9 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       ptx::prefetch_tmap(&tmA);
       ptx::prefetch_tmap(&tmW);
       ptx::mbar_expect_tx(wbar, 2 * a.w_bytes);
-      if (a.w3d) {   // long rows: (BN*EPC, planes, taps)
+      if (a.stack) {  // (BN*EPC, hi/lo, planes, taps) -> smem [tap][plane][hi BN rows | lo BN rows]
+        ptx::tma_load_4d(wsm, &tmW, wbar, nt * a.BN * kEPC, 0, 0, 0);
+      } else if (a.w3d) {   // long rows: (BN*EPC, planes, taps)
         ptx::tma_load_3d(wsm, &tmW, wbar, nt * a.BN * kEPC, 0, 0);                 // hi: taps [0, taps)
         ptx::tma_load_3d(wsm + a.w_bytes, &tmW, wbar, nt * a.BN * kEPC, 0, a.taps);  // lo: taps [taps, 2 taps)
       } else {
@@ -187,8 +192,11 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     const uint32_t idesc = ptx::idesc_mma(128, a.BN, 0, 0, 2);
+    const uint32_t idesc2 = ptx::idesc_mma(128, 2 * a.BN, 0, 0, 2);
     const uint32_t wtap = (uint32_t)planes_w * a.BN * 16;     // weight bytes per tap (hi)
     const uint64_t wdesc = ptx::smem_desc(ptx::smem_u32(wsm), a.BN * 16, 128);
+    const uint32_t pl2 = 2u * a.BN * 16;                      // stacked: bytes per plane (hi + lo rows)
+    const uint64_t wdesc2 = ptx::smem_desc(ptx::smem_u32(wsm), pl2, 128);
     ptx::mbar_wait(wbar, 0);
     int slot = 0;
     uint32_t sph = 0;
@@ -198,14 +206,27 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     for (int m = m0; m < a.n_mtiles; m += mstep) {
       ptx::mbar_wait(&tempty[acc], aph ^ 1);
       if (!(a.knob & 256)) ptx::tc_fence_after();
-      const uint32_t d = tmem + acc * a.BN;
+      const uint32_t d = tmem + acc * a.accw;
       for (int kcc = 0; kcc < a.n_kc; ++kcc) {
         for (int gi = 0; gi < ngrp; ++gi) {
           ptx::mbar_wait(&afull[slot], sph);
           if (!(a.knob & 256)) ptx::tc_fence_after();
           if (lane == 0) TSL(4, dbg_i[4]++);
           if (ptx::elect_one()) {
-            if (!(a.knob & 2)) {
+            if (!(a.knob & 2) && a.stack) {
+#pragma unroll
+            for (int i = 0; i < TPS; ++i) {
+              const int t = gi * TPS + i;
+              const uint32_t ahi = tmem + a_col0 + (slot * TPS + i) * 2 * KC;
+              const uint64_t bt = ptx::desc_add(wdesc2, t * planes_w * pl2 + kcc * (KC / kEPC) * pl2);
+#pragma unroll
+              for (int kk = 0; kk < KC / 8; ++kk) {
+                const uint64_t bd = ptx::desc_add(bt, 2 * kk * pl2);
+                ptx::umma_tf32_ts(d, ahi + kk * 8, bd, idesc2, (kcc | t | kk) ? 1u : 0u);   // [hi*hi | hi*lo]
+                ptx::umma_tf32_ts(d, ahi + KC + kk * 8, bd, idesc, 1u);                    // lo*hi
+              }
+            }
+            } else if (!(a.knob & 2)) {
             // one slot = tps taps x (KC hi + KC lo columns): 3 x KC/8 x tps MMAs per handshake
             // compile-time trip counts: the elected lane's block is straight-line code (a runtime
             // loop here costs an R2UR round trip per tcgen05.mma, ~4x the small-N MMA time)
@@ -358,7 +379,15 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         if (a.knob & 64) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) u[i] = 0.f;
-        } else ptx::tmem_ld16(tmem + lane_addr + acc * a.BN + g * 16, u);
+        } else {
+          ptx::tmem_ld16(tmem + lane_addr + acc * a.accw + g * 16, u);
+          if (a.stack) {                   // + the A_hi*W_lo half
+            float u2[16];
+            ptx::tmem_ld16(tmem + lane_addr + acc * a.accw + a.BN + g * 16, u2);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) u[i] += u2[i];
+          }
+        }
         if (g == ng - 1) {
           if (!(a.knob & 256)) ptx::tc_fence_before();
           __syncwarp();
@@ -504,6 +533,9 @@ static bool ts_plan(const ConvSpec& c, TsArgs& a, int& kc) {
   if (a.BN == 0) return false;
   a.n_ntiles = c.Coutp / a.BN;
   a.w_bytes = (uint32_t)a.taps * c.Cinp * a.BN * 4;
+  static const bool stack_on = [] { const char* e = std::getenv("PST_TS_STACK"); return e == nullptr || e[0] != '0'; }();
+  a.stack = (stack_on && a.BN * kEPC <= 256) ? 1 : 0;
+  a.accw = a.stack ? 2 * a.BN : a.BN;
   const int fixed = 2 * (int)a.w_bytes + 4 * 32 * 17 * 4 + 2048 + (2 * kMaxBand + 2 * kMaxSlots + 2 * kMaxAcc + 1) * 8 + 16 + 256;
   a.band_stages = std::min(kMaxBand, (227 * 1024 - 1024 - fixed) / (int)a.band_bytes);
   if (a.band_stages < 2) return false;
@@ -517,12 +549,12 @@ static bool ts_plan(const ConvSpec& c, TsArgs& a, int& kc) {
       if (force_nacc && nacc != force_nacc) continue;
       // a set may reuse a slot only after the group kTsSets earlier completed its own wait on it
       // (mbarrier parity aliasing): n_slots >= kTsSets
-      if ((512 - nacc * a.BN) / (2 * kc * tps) >= std::max(nacc > 2 ? 3 : 2, kTsSets)) { a.n_acc = nacc; break; }
+      if ((512 - nacc * a.accw) / (2 * kc * tps) >= std::max(nacc > 2 ? 3 : 2, kTsSets)) { a.n_acc = nacc; break; }
     }
     if (a.n_acc) { a.tps = tps; break; }
   }
   if (a.tps == 0) return false;
-  a.n_slots = std::min(kMaxSlots, (512 - a.n_acc * a.BN) / (2 * kc * a.tps));
+  a.n_slots = std::min(kMaxSlots, (512 - a.n_acc * a.accw) / (2 * kc * a.tps));
   if (a.n_slots < std::max(2, kTsSets)) return false;
   return true;
 }
@@ -552,7 +584,15 @@ bool conv_ts(const ConvSpec& c, cudaStream_t st) {
   // weights: shadow [2 (hi, lo)][taps][Cinp/EPC][Coutp][EPC] viewed as (EPC, Coutp, Cinp/EPC, 2 taps)
   CUtensorMap tW;
   a.w3d = a.BN * kEPC <= 256 ? 1 : 0;
-  if (a.w3d) {
+  if (a.stack) {
+    // the shadow is [2 (hi, lo)][taps][Cinp/EPC][Coutp][EPC]; view it as (Coutp*EPC, hi/lo,
+    // planes, taps) so one box lands as [tap][plane][hi rows | lo rows] in shared memory
+    const uint64_t plane_b = (uint64_t)c.Coutp * 16, tap_b = (uint64_t)(c.Cinp / kEPC) * plane_b;
+    uint64_t wd[4] = {(uint64_t)c.Coutp * kEPC, 2, (uint64_t)c.Cinp / kEPC, (uint64_t)a.taps};
+    uint64_t ws[3] = {tap_b * a.taps, plane_b, tap_b};
+    uint32_t wb[4] = {(uint32_t)(a.BN * kEPC), 2, (uint32_t)(c.Cinp / kEPC), (uint32_t)a.taps};
+    tW = make_tmap(act_tmap_dtype(), 4, c.wshadow, wd, ws, wb, nullptr);
+  } else if (a.w3d) {
     uint64_t wd[3] = {(uint64_t)c.Coutp * kEPC, (uint64_t)c.Cinp / kEPC, (uint64_t)(2 * a.taps)};
     uint64_t ws[2] = {(uint64_t)c.Coutp * 16, (uint64_t)(c.Cinp / kEPC) * c.Coutp * 16};
     uint32_t wb[3] = {(uint32_t)(a.BN * kEPC), (uint32_t)(c.Cinp / kEPC), (uint32_t)a.taps};
