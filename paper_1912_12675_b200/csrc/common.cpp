@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // common.cpp -- tensor-map encoding and device queries.
 #include "common.h"
@@ -46,6 +47,12 @@ CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void* gaddr, const
     throw CudaError(msg);
   }
   return m;
+}
+
+int wgrad_sms(int device) {
+  static const int over = [] { const char* e = std::getenv("PST_WG_SMS"); return e ? std::atoi(e) : 0; }();
+  const int n = num_sms(device);
+  return over > 0 ? std::min(over, n) : n;
 }
 
 int num_sms(int device) {
@@ -110,6 +117,7 @@ void read(int cls, double* ms, int64_t* n, double* bytes, double* flops) {
 }  // namespace pst
 
 namespace pst {
+thread_local bool pdl_suppressed = false;
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PST_PDL");

@@ -117,6 +117,9 @@ CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void* gaddr, const
                       const uint32_t* estrides);
 
 int num_sms(int device);
+// SMs the weight-gradient kernels plan their split-K grid for (PST_WG_SMS; default all): the
+// wgrad runs on a forked stream beside the dgrad, so it can be given part of the GPU.
+int wgrad_sms(int device);
 
 // Launch accounting and optional per-kernel CUDA-event timing (bench.py's roofline).
 // ---------------------------------------------------------------- programmatic dependent launch
@@ -128,6 +131,9 @@ int num_sms(int device);
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();
+// Launches of this thread skip the programmatic-dependent-launch attribute while set (the forked
+// wgrad stream: its next kernel's CTAs must not sit on SMs waiting while the dgrad needs them).
+extern thread_local bool pdl_suppressed;
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                             Args... args) {
@@ -140,7 +146,7 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = (pdl_enabled() && !pdl_suppressed) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 

@@ -1243,7 +1243,7 @@ void conv_wgrad_tc(const WgradSpec& w, cudaStream_t st) {
 #if PST_SPLIT
   int dev_b;
   PST_CUDA(cudaGetDevice(&dev_b));
-  WbArgs b = plan_band(w.N, w.H, w.W, w.Cinp, w.Ho, w.Wo, w.Coutp, w.k, w.S, w.pad, num_sms(dev_b));
+  WbArgs b = plan_band(w.N, w.H, w.W, w.Cinp, w.Ho, w.Wo, w.Coutp, w.k, w.S, w.pad, wgrad_sms(dev_b));
   if (b.G >= 1) {
     PST_CHECK_ARG(b.ksplit == w.ksplit, "wgrad: workspace planned for a different split");
     b.part = w.part;

@@ -622,7 +622,8 @@ bool conv_ts(const ConvSpec& c, cudaStream_t st) {
   PST_CUDA(cudaGetDevice(&dev));
   const int sms = num_sms(dev);
   const int total = a.n_mtiles * a.n_ntiles;
-  const int grid = std::min(total, std::max(a.n_ntiles, (sms / a.n_ntiles) * a.n_ntiles));
+  const int cap = c.max_ctas > 0 ? std::min(c.max_ctas, sms) : sms;
+  const int grid = std::min(total, std::max(a.n_ntiles, (cap / a.n_ntiles) * a.n_ntiles));
   const double es = sizeof(act_t);
   const double bytes = (double)c.N * c.H * c.W * c.Cinp * es +
                        (double)c.N * c.Ho * c.Wo * c.Coutp * (c.epi == EPI_BIAS_F32 ? 4.0 : es) +

@@ -362,7 +362,7 @@ bool conv_wgrad_ts(const WgradSpec& w, cudaStream_t st) {
   int dev;
   PST_CUDA(cudaGetDevice(&dev));
   WtArgs a;
-  if (!wgrad_ts_plan(w.N, w.H, w.W, w.Cinp, w.Ho, w.Wo, w.Coutp, w.k, w.S, w.pad, num_sms(dev), &a)) return false;
+  if (!wgrad_ts_plan(w.N, w.H, w.W, w.Cinp, w.Ho, w.Wo, w.Coutp, w.k, w.S, w.pad, wgrad_sms(dev), &a)) return false;
   PST_CHECK_ARG(a.ksplit == w.ksplit, "wgrad: workspace planned for a different split");
   a.part = w.part;
   a.dbg = w.dbg;

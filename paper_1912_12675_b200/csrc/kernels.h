@@ -25,6 +25,7 @@ struct ConvSpec {
   int Ho, Wo, Coutp, Cout;
   int k, S;                 // kernel size, input element stride
   int off, sgn;             // input coord = out*S + off + sgn*tap  (fwd: -pad,+1; dgrad: +pad,-1)
+  int max_ctas;             // grid cap (0: all SMs) -- the dgrad shares the GPU with the forked wgrad
   const act_t* wshadow;     // [k*k][Coutp][Cinp]
   int epi;                  // EpiMode
   int relu;

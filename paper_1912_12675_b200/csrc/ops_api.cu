@@ -128,7 +128,7 @@ int pst_op_conv2d_wgrad(const float* x, const float* gy, float* gw, int N, int C
     input_to_act(gy, ga, N, Cout, g.Ho, g.Wo, g.Coutp, 0);
     int dev;
     PST_CUDA(cudaGetDevice(&dev));
-    WgradPlan p = wgrad_plan(N, H, W, g.Cinp, g.Ho, g.Wo, g.Coutp, k, stride, pad, num_sms(dev));
+    WgradPlan p = wgrad_plan(N, H, W, g.Cinp, g.Ho, g.Wo, g.Coutp, k, stride, pad, wgrad_sms(dev));
     float* part = s.get<float>((size_t)p.part_floats);
     WgradSpec wg{};
     wg.x = xa; wg.N = N; wg.H = H; wg.W = W; wg.Cinp = g.Cinp;
@@ -176,7 +176,7 @@ extern "C" int pst_op_time_conv(int which, int N, int Cin, int H, int W, int Cou
     double* stats = s.get<double>((size_t)2 * g.Coutp);
     int dev;
     PST_CUDA(cudaGetDevice(&dev));
-    WgradPlan p = wgrad_plan(N, H, W, g.Cinp, g.Ho, g.Wo, g.Coutp, k, stride, pad, num_sms(dev));
+    WgradPlan p = wgrad_plan(N, H, W, g.Cinp, g.Ho, g.Wo, g.Coutp, k, stride, pad, wgrad_sms(dev));
     float* part = which == 2 ? s.get<float>((size_t)p.part_floats) : nullptr;
     auto launch = [&] {
       if (which == 0) {

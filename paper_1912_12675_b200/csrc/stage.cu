@@ -98,7 +98,7 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     if (li.S == 2 && need_gin)
       b.dil = alloc<act_t>((size_t)B * li.in_H * li.in_W * li.Coutp, false);
     const int kk = li.kk;
-    WgradPlan wp = wgrad_plan(B, li.in_H, li.in_W, li.Cinp, li.Ho, li.Wo, li.Coutp, kk, li.S, li.pad, nsm);
+    WgradPlan wp = wgrad_plan(B, li.in_H, li.in_W, li.Cinp, li.Ho, li.Wo, li.Coutp, kk, li.S, li.pad, wgrad_sms(dev));
     b.ksplit = wp.ksplit;
     b.wpart = alloc<float>((size_t)wp.part_floats, false);
     // weight shadows (+ the 3xTF32 lo plane right after the raw plane in the split build)
@@ -366,7 +366,10 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
       if (side_wgrad()) {
         PST_CUDA(cudaEventRecord(ev_fork, st));
         PST_CUDA(cudaStreamWaitEvent(wstream, ev_fork, 0));
+        static const bool wg_pdl = [] { const char* e = std::getenv("PST_WG_PDL"); return e == nullptr || e[0] != '0'; }();
+        pdl_suppressed = !wg_pdl;
         conv_wgrad_tc(wg, wstream);
+        pdl_suppressed = false;
       } else {
         conv_wgrad_tc(wg, st);
       }
@@ -414,6 +417,8 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
         c.res_mode = e.res_mode;
         c.res_H = e.Ho; c.res_W = e.Wo; c.res_C = e.Coutp; c.res_pad = e.res_pad;
       }
+      static const int dg_ctas = [] { const char* e = std::getenv("PST_DG_CTAS"); return e ? std::atoi(e) : 0; }();
+      c.max_ctas = side_wgrad() ? dg_ctas : 0;
       if (!skip("dgrad")) conv_tc(c, st);
     }
   }
