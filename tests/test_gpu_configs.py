@@ -51,10 +51,10 @@ def pst():
     return p
 
 
-def _run(pst, name, K, B, N, check, lr=None, **kw):
+def _run(pst, name, K, B, N, check, lr=None, ppv=None, **kw):
     cfg = W.CONFIGS[name]
     lrv = cfg.lr_vector(K) if lr is None else [lr] * K
-    r = run_both(pst, cfg.netspec(), cfg.ppv[K], B, N, lrv, lr_np=lrv[-1],
+    r = run_both(pst, cfg.netspec(), cfg.ppv[K] if ppv is None else ppv, B, N, lrv, lr_np=lrv[-1],
                  mom=cfg.momentum, wd=cfg.weight_decay, milestones=cfg.milestones, check=check, **kw)
     worst, lerr, vers, _ = r
     assert worst[0] <= W_TOL, worst
@@ -82,9 +82,15 @@ def test_resnet110_b128_k1(pst):
 
 
 def test_resnet110_b128_k2(pst):
-    """The paper's 2-GPU case: ResNet-110, batch 128, PPV (37); mini-batch 3 is the
+    """The paper's 2-GPU case with the paper's own PPV (37); mini-batch 3 is the
     first whose stage-0 forward reads a stale version (1, staleness 2)."""
-    _run(pst, "resnet110", 2, 128, 4, check={2, 3}, lr=0.01, stage_level=True)
+    _run(pst, "resnet110", 2, 128, 4, check={2, 3}, lr=0.01, stage_level=True,
+         ppv=W.CONFIGS["resnet110"].paper_ppv[2])
+
+
+def test_resnet110_k2_balanced_ppv(pst):
+    """bench.py's 2-GPU partition: the profile-balanced PPV (47) (pst_workloads/balance.py)."""
+    _run(pst, "resnet110", 2, 32, 4, check={3}, lr=0.01, stage_level=True)
 
 
 def test_resnet110_k4(pst):
