@@ -90,7 +90,7 @@ def test_resnet110_b128_k2(pst):
 
 def test_resnet110_k2_balanced_ppv(pst):
     """bench.py's 2-GPU partition: the profile-balanced PPV (47) (pst_workloads/balance.py)."""
-    _run(pst, "resnet110", 2, 32, 4, check={3}, lr=0.01, stage_level=True)
+    _run(pst, "resnet110", 2, 32, 4, check={3}, lr=0.001, stage_level=True)
 
 
 def test_resnet110_k4(pst):
