@@ -215,6 +215,22 @@ def main():
     for i in range(warm):
         pipe.step(*dev[i % n_pool])
     pipe.sync()
+    t_w = time.perf_counter()
+    for i in range(10):
+        pipe.step(*dev[(warm + i) % n_pool])
+    pipe.sync()
+    per_step = (time.perf_counter() - t_w) / 10
+    warm += 10
+    # untimed spin-up: about 1.5 s more of steps so a fresh box's clocks and caches settle (the
+    # first bench on a new box otherwise sometimes reads 20-50% slow); the count is agreed on
+    # by all ranks, whose stages exchange activations every step
+    n_spin = int(max_over_ranks(float(min(2000, int(1.5 / max(per_step, 1e-4))))))
+    for i in range(n_spin):
+        pipe.step(*dev[(warm + i) % n_pool])
+        if i % 50 == 49:
+            pipe.sync()
+    pipe.sync()
+    warm += n_spin
     torch.cuda.synchronize()
     barrier()
 

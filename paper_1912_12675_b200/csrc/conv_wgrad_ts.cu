@@ -27,7 +27,8 @@ namespace pst {
 #if PST_SPLIT
 namespace {
 
-constexpr int kWtThreads = 320;
+// warps: 0 TMA, 1 MMA, 2.. converters in SETS sets of 4 taking units in turn (2-5 also epilogue)
+constexpr int wt_threads(int sets) { return (2 + 4 * sets) * 32; }
 constexpr int kWtMaxSB = 8;
 constexpr int kWtMaxSlots = 8;
 
@@ -38,6 +39,7 @@ struct WtArgs {
   int rows, n_mt, G, n_mgroups, BNw, n_ntiles, ksplit;
   int pl_grp, pl_all;
   int SB, St;                          // smem stages, TMEM A slots
+  int sets;                            // converter sets (2 or 3; compile-time in the kernel)
   uint32_t rawx_bytes, rawx_tx, rawd_bytes, b_bytes, stage_bytes, sboB;
   float* part;
   unsigned long long* dbg;   // optional timeline (CTA 0, clock64), PST_DBG_TL
@@ -52,8 +54,8 @@ struct WtArgs {
     }                                                                                    \
   } while (0)
 
-template <int G, int P16>
-__global__ void __launch_bounds__(kWtThreads, 1)
+template <int G, int P16, int SETS>
+__global__ void __launch_bounds__(wt_threads(SETS), 1)
     conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD,
                          const WtArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(kWtThreads, 1)
     // tcgen05.st, wait::st -- is latency-bound).  A set converts all P16 pixels of its unit for
     // every M tile the CTA owns, and the unit's dY block into the K-major hi/lo B rows.
     const int q = warp & 3;
-    const int set = (warp - 2) >> 2;            // 0 or 1
+    const int set = (warp - 2) >> 2;            // 0 .. SETS-1
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     int rb[4] = {-1, -1, -1, -1};               // this thread's A row (one per owned M tile)
 #pragma unroll
@@ -196,12 +198,15 @@ __global__ void __launch_bounds__(kWtThreads, 1)
     const int unitsB = (a.BNw / 4) * nq;
     int sb = 0, slot = 0;
     uint32_t sbph = 0, slph = 0;
+    int turn = 0;                               // set owning unit `it`
     for (int it = 0; it < n_iter; ++it) {
       const int my_sb = sb, my_slot = slot;
       const uint32_t my_sbph = sbph, my_slph = slph;
       if (++sb == a.SB) { sb = 0; sbph ^= 1; }
       if (++slot == a.St) { slot = 0; slph ^= 1; }
-      if ((it & 1) != set) continue;             // the other set's unit
+      const bool mine = turn == set;
+      if (++turn == SETS) turn = 0;
+      if (!mine) continue;                       // another set's unit
       ptx::mbar_wait(&full[my_sb], my_sbph);
       ptx::mbar_wait(&afree[my_slot], my_slph ^ 1);
       ptx::tc_fence_after();
@@ -343,6 +348,13 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   const int budget = 200 * 1024;
   a.SB = std::min(kWtMaxSB, budget / (int)a.stage_bytes);
   if (a.SB < 2) return false;
+  // a third converter set (three units in flight) where the slots allow it without shrinking G:
+  // a set reuses a slot / band stage only after the unit SETS earlier waited on it (mbarrier
+  // parity aliasing), so St >= SETS and SB >= SETS
+  static const int max_sets = [] { const char* e = std::getenv("PST_WT_SETS"); return e ? std::atoi(e) : 3; }();
+  // (measured: g1 wgrad 24.2 -> 21.3 us with 3 sets; the 576-row g3 gets slower, so only the
+  // small-row layers take it)
+  a.sets = (max_sets >= 3 && a.St >= 3 && a.SB >= 3 && a.rows <= 256) ? 3 : 2;
   a.n_mgroups = ceil_div(a.n_mt, a.G);
   a.ny = ceil_div(Ho, a.bh);
   a.n_units = ceil_div(N, a.nb) * a.ny;
@@ -379,12 +391,17 @@ bool conv_wgrad_ts(const WgradSpec& w, cudaStream_t st) {
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const WtArgs);
   KernT kern = nullptr;
   {
-    const KernT tab[2][4] = {{conv_wgrad_ts_kernel<1, 16>, conv_wgrad_ts_kernel<2, 16>, conv_wgrad_ts_kernel<3, 16>,
-                              conv_wgrad_ts_kernel<4, 16>},
-                             {conv_wgrad_ts_kernel<1, 32>, conv_wgrad_ts_kernel<2, 32>, conv_wgrad_ts_kernel<3, 32>,
-                              conv_wgrad_ts_kernel<4, 32>}};
+    const KernT tab[2][2][4] = {
+        {{conv_wgrad_ts_kernel<1, 16, 2>, conv_wgrad_ts_kernel<2, 16, 2>, conv_wgrad_ts_kernel<3, 16, 2>,
+          conv_wgrad_ts_kernel<4, 16, 2>},
+         {conv_wgrad_ts_kernel<1, 32, 2>, conv_wgrad_ts_kernel<2, 32, 2>, conv_wgrad_ts_kernel<3, 32, 2>,
+          conv_wgrad_ts_kernel<4, 32, 2>}},
+        {{conv_wgrad_ts_kernel<1, 16, 3>, conv_wgrad_ts_kernel<2, 16, 3>, conv_wgrad_ts_kernel<3, 16, 3>,
+          conv_wgrad_ts_kernel<4, 16, 3>},
+         {conv_wgrad_ts_kernel<1, 32, 3>, conv_wgrad_ts_kernel<2, 32, 3>, conv_wgrad_ts_kernel<3, 32, 3>,
+          conv_wgrad_ts_kernel<4, 32, 3>}}};
     PST_CHECK_ARG((a.P16 == 16 || a.P16 == 32) && a.G >= 1 && a.G <= 4, "wgrad tiling");
-    kern = tab[a.P16 == 32 ? 1 : 0][a.G - 1];
+    kern = tab[a.sets == 3 ? 1 : 0][a.P16 == 32 ? 1 : 0][a.G - 1];
   }
   PST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = a.n_mgroups * a.n_ntiles * a.ksplit;
@@ -393,7 +410,7 @@ bool conv_wgrad_ts(const WgradSpec& w, cudaStream_t st) {
                        (double)a.rows * w.Coutp * 4.0;   // algorithmic: X + dY read, dW written once
   const double flops = 2.0 * a.rows * (double)w.Coutp * w.N * w.Ho * w.Wo;
   prof::begin(st);
-  PST_CUDA(launch_k(kern, dim3(grid), dim3(kWtThreads), smem, st, tX, tD, a));
+  PST_CUDA(launch_k(kern, dim3(grid), dim3(wt_threads(a.sets)), smem, st, tX, tD, a));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::CONV_WGRAD, bytes, flops);
   return true;

@@ -103,14 +103,32 @@ def test_resnet110_k8(pst):
 
 def test_resnet362_hybrid_k8(pst):
     """configs[4]: 8 stages, pipelined for 2 epochs of 5 steps, drain, then non-pipelined
-    (AMB-10); SURVEY 8(d)'s parity recipe shortened to 15 mini-batches, at batch 16.
-    lr 1e-4: at batch 16 the 362-layer net starts at loss 18.6 and the exact trajectory is
-    chaotic at 1e-3 (a 1e-7 initial perturbation moves the oracle's own stage-0 weights by 33%
-    in 15 mini-batches; by 9e-5 at 1e-4 -- DESIGN.md AMB-21c)."""
+    (AMB-10) -- SURVEY 8(d)'s parity recipe shortened to 12 mini-batches, at batch 16 and
+    lr 1e-4.  At batch 16 the 362-layer net starts at loss 18.6 and its exact trajectory is
+    sensitive at the float32 level: a 1e-7 relative perturbation of the initial weights moves the
+    fp64 oracle's own stage-0 weights by 4e-4 and its first non-pipelined loss by 3.6e-3 (DESIGN.md
+    AMB-21c).  The weight tolerance is therefore max(2e-3, 10 x that spread), the spread measured
+    here by running the oracle a second time from the perturbed weights (reading AMB-21d)."""
+    import numpy as np
+    from tests.parity import flat_params, hparams, oracle_run, stage_errors
     cfg = W.CONFIGS["resnet362"]
     spe = cfg.steps_per_epoch
-    _run(pst, "resnet362", 8, 16, 15, check=None, per_step=False, n_p=cfg.hybrid_epoch * spe, spe=spe,
-         lr=1e-4, stage_level=True)
+    K, B, N, lr = 8, 16, 12, 1e-4
+    net, ppv = cfg.netspec(), cfg.ppv[K]
+    n_p = cfg.hybrid_epoch * spe
+    hp = hparams([lr] * K, K, lr, cfg.momentum, cfg.weight_decay, cfg.milestones, 0.1, spe)
+    flat = W.init_params(net, seed=5)
+    data = W.batches(net.in_shape, B, N, seed=105)
+    pert = flat.astype(np.float64) * (1 + 1e-7 * np.random.default_rng(0).standard_normal(flat.shape))
+    ref = oracle_run(net, flat, ppv, data, hp, n_p=n_p)
+    ref_p = oracle_run(net, pert, ppv, data, hp, n_p=n_p)
+    spread = stage_errors(net, ppv, flat_params(net, ref_p.params), flat_params(net, ref.params))[0]
+    worst, lerr, vers, _ = run_both(pst, net, ppv, B, N, [lr] * K, lr_np=lr, mom=cfg.momentum,
+                                    wd=cfg.weight_decay, milestones=cfg.milestones, n_p=n_p, spe=spe,
+                                    per_step=False, stage_level=True)
+    assert worst[0] <= max(W_TOL, 10 * spread), (worst, spread)
+    assert lerr <= L_TOL, lerr
+    assert list(vers) == [N] * K
 
 
 def test_lenet5_loss_trajectory_100_steps(pst):
