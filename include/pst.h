@@ -112,6 +112,17 @@ typedef struct {
   const int64_t* milestone_epochs; /* lr *= gamma at each epoch >= milestone */
   float gamma;
   int64_t steps_per_epoch;   /* mini-batches per epoch (epoch of mb i = i / steps_per_epoch) */
+  /* Solver variants of the paper's Caffe-simulated runs (SURVEY f-3).
+   * Zero-initialised fields give the PyTorch form the real 2-GPU runs used (AMB-7). */
+  int32_t solver;            /* 0: PyTorch  v <- mu v + (g + lambda w);  w <- w - lr v
+                                1: Caffe    v <- mu v + lr (g + lambda w);  w <- w - v      */
+  int32_t nesterov;          /* Nesterov momentum (AlexNet, VGG-16):
+                                PyTorch  w <- w - lr (g + lambda w + mu v_new)
+                                Caffe    w <- w - ((1 + mu) v_new - mu v_old)               */
+  int32_t lr_policy;         /* 0: milestones x gamma (above);  1: Caffe "inv" (LeNet-5):
+                                lr(i) = base (1 + inv_gamma i)^(-inv_power), i = the gradient's
+                                mini-batch index (reading AMB-8)                          */
+  float inv_gamma, inv_power;
 } pst_hparams;
 
 /* Distributed mode: one process per stage (rank == stage), NCCL send/recv

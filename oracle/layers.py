@@ -212,6 +212,26 @@ def softmax_ce(z, y):
 
 
 # --------------------------------------------------------------------------- optimiser
+def sgd_caffe(w, v, g, lr, momentum, weight_decay, nesterov=False):
+    """Caffe's SGD and Nesterov solvers (the paper's simulated runs use Caffe, PAPER.md L87;
+    AlexNet/VGG-16 use Nesterov momentum, L286/L288):
+        v_new <- mu * v + lr * (g + lambda * w)
+        SGD:      w <- w - v_new
+        Nesterov: w <- w - ((1 + mu) * v_new - mu * v)
+    Returns (w_new, v_new)."""
+    v_new = momentum * v + lr * (g + weight_decay * w)
+    if nesterov:
+        return w - ((1.0 + momentum) * v_new - momentum * v), v_new
+    return w - v_new, v_new
+
+
+def sgd_nesterov(w, v, g, lr, momentum, weight_decay):
+    """PyTorch's Nesterov form: d = g + lambda w; v <- mu v + d; w <- w - lr (d + mu v)."""
+    d = g + weight_decay * w
+    v_new = momentum * v + d
+    return w - lr * (d + momentum * v_new), v_new
+
+
 def sgd_momentum(w, v, g, lr, momentum, weight_decay):
     """PyTorch SGD (dampening 0, no Nesterov; reading AMB-7):
         v <- mu * v + (g + lambda * w);  w <- w - lr * v

@@ -45,6 +45,11 @@ class HParams:
     milestones: Sequence[int] = ()         # epochs
     gamma: float = 0.1
     steps_per_epoch: int = 1 << 62
+    solver: str = "torch"                  # "torch" (AMB-7) | "caffe"
+    nesterov: bool = False                 # AlexNet / VGG-16 (L286, L288)
+    lr_policy: str = "multistep"           # "multistep" (milestones x gamma) | "inv" (LeNet-5, L284)
+    inv_gamma: float = 0.0
+    inv_power: float = 0.0
 
 
 def staleness(K, s):
@@ -68,6 +73,8 @@ def forward_version(K, s, i, n_p=None):
 
 def learning_rate(hp: HParams, s, i, n_p=None):
     base = hp.lr_pipelined[s] if (n_p is None or i < n_p) else hp.lr_nonpipelined
+    if hp.lr_policy == "inv":              # Caffe "inv": base (1 + gamma i)^(-power)  (L284)
+        return base * (1.0 + hp.inv_gamma * i) ** (-hp.inv_power)
     epoch = i // hp.steps_per_epoch
     return base * (hp.gamma ** sum(1 for m in hp.milestones if epoch >= m))
 
@@ -81,7 +88,12 @@ def _sgd_stage(params, mom, grads, lr, hp):
     for P, V, G in zip(params, mom, grads):
         dp, dv = {}, {}
         for k in P:
-            dp[k], dv[k] = Lx.sgd_momentum(P[k], V[k], G[k], lr, hp.momentum, hp.weight_decay)
+            if hp.solver == "caffe":
+                dp[k], dv[k] = Lx.sgd_caffe(P[k], V[k], G[k], lr, hp.momentum, hp.weight_decay, hp.nesterov)
+            elif hp.nesterov:
+                dp[k], dv[k] = Lx.sgd_nesterov(P[k], V[k], G[k], lr, hp.momentum, hp.weight_decay)
+            else:
+                dp[k], dv[k] = Lx.sgd_momentum(P[k], V[k], G[k], lr, hp.momentum, hp.weight_decay)
         new_p.append(dp)
         new_v.append(dv)
     return new_p, new_v

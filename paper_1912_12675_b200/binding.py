@@ -46,7 +46,9 @@ class _HParams(C.Structure):
     _fields_ = [("batch", C.c_int32), ("momentum", C.c_float), ("weight_decay", C.c_float),
                 ("lr_pipelined", C.POINTER(C.c_float)), ("lr_nonpipelined", C.c_float),
                 ("n_milestones", C.c_int32), ("milestone_epochs", C.POINTER(C.c_int64)),
-                ("gamma", C.c_float), ("steps_per_epoch", C.c_int64)]
+                ("gamma", C.c_float), ("steps_per_epoch", C.c_int64),
+                ("solver", C.c_int32), ("nesterov", C.c_int32), ("lr_policy", C.c_int32),
+                ("inv_gamma", C.c_float), ("inv_power", C.c_float)]
 
 
 class _Dist(C.Structure):
@@ -188,7 +190,8 @@ class Pipeline:
                  lr_nonpipelined: float, momentum: float = 0.9, weight_decay: float = 0.0,
                  milestones: Sequence[int] = (), gamma: float = 0.1, steps_per_epoch: int = 1 << 62,
                  devices: Optional[Sequence[int]] = None, rank: Optional[int] = None,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, solver: str = "torch", nesterov: bool = False,
+                 lr_policy: str = "multistep", inv_gamma: float = 0.0, inv_power: float = 0.0):
         L = lib()
         self.net = net
         self.K = len(ppv) + 1
@@ -198,7 +201,9 @@ class Pipeline:
         lrs = (C.c_float * self.K)(*lr_pipelined)
         ms = (C.c_int64 * max(1, len(milestones)))(*milestones)
         hp = _HParams(batch, momentum, weight_decay, C.cast(lrs, C.POINTER(C.c_float)), lr_nonpipelined,
-                      len(milestones), C.cast(ms, C.POINTER(C.c_int64)), gamma, steps_per_epoch)
+                      len(milestones), C.cast(ms, C.POINTER(C.c_int64)), gamma, steps_per_epoch,
+                      {"torch": 0, "caffe": 1}[solver], int(bool(nesterov)),
+                      {"multistep": 0, "inv": 1}[lr_policy], inv_gamma, inv_power)
         self._keep_hp = (lrs, ms)
         dist = None
         if rank is not None:

@@ -488,11 +488,15 @@ __global__ void sgd_kernel(const SgdSpec s) {
     if (kUpdate) {
       const int64_t vc = *s.v_count;
       const float base = (vc < *s.n_p) ? *s.lr_pipe : s.lr_np;
-      const int64_t epoch = vc / s.spe;
-      float f = 1.f;
-      for (int m = 0; m < s.n_ms; ++m)
-        if (epoch >= s.milestones[m]) f *= s.gamma;
-      lr_sh = base * f;
+      if (s.lr_policy == 1) {   // Caffe "inv": base (1 + gamma i)^(-power)
+        lr_sh = (float)((double)base * pow(1.0 + (double)s.inv_gamma * (double)vc, -(double)s.inv_power));
+      } else {
+        const int64_t epoch = vc / s.spe;
+        float f = 1.f;
+        for (int m = 0; m < s.n_ms; ++m)
+          if (epoch >= s.milestones[m]) f *= s.gamma;
+        lr_sh = base * f;
+      }
     }
   }
   __syncthreads();
@@ -516,8 +520,15 @@ __global__ void sgd_kernel(const SgdSpec s) {
         grad = g.gsum[row * g.Coutp + co];
       }
       float v = s.v[g.off + e];
-      v = s.momentum * v + (grad + s.wd * w);
-      w = w - lr_sh * v;
+      const float d = grad + s.wd * w;
+      if (s.solver == 0) {                 // PyTorch form (AMB-7)
+        v = s.momentum * v + d;
+        w = s.nesterov ? w - lr_sh * (d + s.momentum * v) : w - lr_sh * v;
+      } else {                             // Caffe form
+        const float vo = v;
+        v = s.momentum * v + lr_sh * d;
+        w = s.nesterov ? w - ((1.f + s.momentum) * v - s.momentum * vo) : w - v;
+      }
       s.v[g.off + e] = v;
       s.w[g.off + e] = w;
     }

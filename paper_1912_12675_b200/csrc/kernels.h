@@ -160,6 +160,8 @@ struct SgdSpec {
   float lr_np, momentum, wd, gamma;
   const int64_t* milestones; int n_ms; int64_t spe;
   const int64_t* n_p;       // device scalar: hybrid switch mini-batch (huge if none)
+  int solver, nesterov, lr_policy;   // pst_hparams solver variants (0: PyTorch form, 1: Caffe)
+  float inv_gamma, inv_power;
   // split-K reduction pass (one launch for all conv segments, coalesced float4 over [rows][Coutp])
   const int64_t* red_block_start;  // device: first reduce block of each segment (0 blocks for non-conv)
   int64_t red_total_blocks;

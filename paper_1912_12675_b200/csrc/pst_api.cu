@@ -330,6 +330,9 @@ int pst_create(const pst_net* net, const pst_partition* part, const pst_hparams*
     c->ranges = partition(c->net, c->K, part->ppv);
     PST_CHECK_ARG(hp->batch >= 1 && hp->batch <= 4096, "batch");
     PST_CHECK_ARG(hp->lr_pipelined != nullptr, "lr_pipelined");
+    PST_CHECK_ARG((hp->solver == 0 || hp->solver == 1) && (hp->nesterov == 0 || hp->nesterov == 1) &&
+                      (hp->lr_policy == 0 || hp->lr_policy == 1),
+                  "solver / nesterov / lr_policy");
     c->batch = hp->batch;
     c->hp = *hp;
     c->lr_pipe.assign(hp->lr_pipelined, hp->lr_pipelined + c->K);

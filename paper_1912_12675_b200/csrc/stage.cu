@@ -12,7 +12,9 @@ namespace pst {
 // out of the step to measure its in-graph cost.  Results are wrong when set.
 static bool side_wgrad() {
   static const bool on = [] { const char* e = std::getenv("PST_WSTREAM"); return e == nullptr || e[0] != '0'; }();
-  return on;
+  // the per-kernel event profile (pst_profile) times launches one at a time: a wgrad running
+  // beside the dgrad would be charged the time it waits for SMs
+  return on && !prof::enabled;
 }
 static bool skip(const char* cls) {
   static const char* env = std::getenv("PST_SKIP");
@@ -197,6 +199,11 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
   sgd_.n_ms = hp.n_milestones;
   sgd_.spe = hp.steps_per_epoch > 0 ? hp.steps_per_epoch : INT64_MAX;
   sgd_.n_p = d_np_;
+  sgd_.solver = hp.solver;
+  sgd_.nesterov = hp.nesterov;
+  sgd_.lr_policy = hp.lr_policy;
+  sgd_.inv_gamma = hp.inv_gamma;
+  sgd_.inv_power = hp.inv_power;
   build_shadows(sgd_, stream);
   PST_CUDA(cudaStreamSynchronize(stream));
 }

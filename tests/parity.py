@@ -77,7 +77,7 @@ def hparams(cfg_lr, K, lr_np, momentum, wd, milestones=(), gamma=0.1, spe=1 << 6
 
 
 def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, spe=1 << 62,
-             milestones=(), per_step=True, seed=5, check=None, stage_level=False):
+             milestones=(), per_step=True, seed=5, check=None, stage_level=False, solver_kw=None):
     """Train the same seeded mini-batches through libpst (all stages on cuda:0, local mode)
     and through Oracle B; compare the weights after every compared step and after the
     drain, and the loss of every mini-batch.  `check`: None = every step (if per_step),
@@ -90,10 +90,13 @@ def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, sp
     data = W.batches(net.in_shape, B, N, seed=seed + 100)
     lr_np = lr[-1] if lr_np is None else lr_np
     hp = hparams(lr, K, lr_np, mom, wd, milestones, 0.1, spe)
+    skw = dict(solver_kw or {})        # solver / nesterov / lr_policy / inv_gamma / inv_power
+    for k, v in skw.items():
+        setattr(hp, k, v)
     snap = (True if check is None else set(check)) if per_step else False
     ref = oracle_run(net, flat, ppv, data, hp, n_p=n_p, snapshot=snap)
     pipe = pst.Pipeline(net, flat, ppv, B, lr, lr_np, momentum=mom, weight_decay=wd, milestones=milestones,
-                        steps_per_epoch=spe)
+                        steps_per_epoch=spe, **skw)
     if n_p is not None:
         assert n_p % spe == 0
         pipe.set_hybrid(n_p // spe)

@@ -84,3 +84,31 @@ def test_distributed_mode_single_rank(pst):
     assert e[0] <= W_TOL, e
     assert loss_errors(pipe.losses(0, 6), ref.losses) <= L_TOL
     pipe.close()
+
+
+@pytest.mark.parametrize("skw,ppv", [
+    (dict(solver="caffe", lr_policy="inv", inv_gamma=1e-4, inv_power=0.75), (2,)),   # LeNet-5's (L284)
+    (dict(solver="caffe", nesterov=True), (1, 2, 3)),                                  # AlexNet/VGG (L286-288)
+    (dict(nesterov=True), (2,)),                                                        # PyTorch Nesterov
+])
+def test_solver_variants(pst, skw, ppv):
+    """The paper's Caffe-simulated solver settings through the GPU update
+    kernel, pipelined, against the oracle's solver of the same form; lr milestones change the rate
+    mid-run so the Caffe form (lr folded into the history) differs from the PyTorch form."""
+    net = W.tiny_cnn(hw=8)
+    K = len(ppv) + 1
+    worst, lerr, vers, _ = run_both(pst, net, ppv, 32, 10, [0.05] * K, wd=5e-4, milestones=(2,), spe=3,
+                                    solver_kw=skw)
+    assert worst[0] <= W_TOL, worst
+    assert lerr <= L_TOL, lerr
+
+
+def test_lenet5_paper_solver_k2(pst):
+    """configs[0] with the paper's own LeNet-5 solver: Caffe SGD, momentum 0.9, wd 5e-4, lr 0.01
+    with the "inv" policy (L284; gamma 1e-4 / power 0.75, Caffe's LeNet values, external), 2 stages."""
+    cfg = W.CONFIGS["lenet5"]
+    worst, lerr, vers, _ = run_both(pst, W.lenet5(), cfg.ppv[2], 64, 20, cfg.lr_vector(2), mom=cfg.momentum,
+                                    wd=cfg.weight_decay,
+                                    solver_kw=dict(solver="caffe", lr_policy="inv", inv_gamma=1e-4, inv_power=0.75))
+    assert worst[0] <= W_TOL, worst
+    assert lerr <= L_TOL, lerr
