@@ -319,12 +319,13 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   a.n_mt = ceil_div(a.rows, 128);
   a.BNw = tile_n16(Coutp, 128);
   a.n_ntiles = Coutp / a.BNw;
-  const int ptarget = 32;
+  // pixels per unit (PST_WT_PTARGET experiments: 64 halves the per-unit hand-offs, needs G = 1)
+  static const int ptarget = [] { const char* e = std::getenv("PST_WT_PTARGET"); return e ? std::atoi(e) : 32; }();
   if (Ho * Wo >= ptarget) { a.nb = 1; a.bh = std::max(1, std::min(Ho, ptarget / Wo)); }
   else { a.nb = std::max(1, std::min(N, ptarget / (Ho * Wo))); a.bh = Ho; }
   a.P = a.nb * a.bh * Wo;
   a.P16 = round_up(a.P, 16);
-  if (a.P16 > 32) return false;   // two converter sets x 16 pixels
+  if (a.P16 != 16 && a.P16 != 32 && a.P16 != 64) return false;
   a.band_r = (a.bh - 1) * S + k;
   a.band_c = (Wo - 1) * S + k;
   if (a.band_c * kEPC > 256 || a.band_r > 256) return false;
@@ -400,8 +401,15 @@ bool conv_wgrad_ts(const WgradSpec& w, cudaStream_t st) {
           conv_wgrad_ts_kernel<4, 16, 3>},
          {conv_wgrad_ts_kernel<1, 32, 3>, conv_wgrad_ts_kernel<2, 32, 3>, conv_wgrad_ts_kernel<3, 32, 3>,
           conv_wgrad_ts_kernel<4, 32, 3>}}};
-    PST_CHECK_ARG((a.P16 == 16 || a.P16 == 32) && a.G >= 1 && a.G <= 4, "wgrad tiling");
-    kern = tab[a.sets == 3 ? 1 : 0][a.P16 == 32 ? 1 : 0][a.G - 1];
+    PST_CHECK_ARG((a.P16 == 16 || a.P16 == 32 || a.P16 == 64) && a.G >= 1 && a.G <= 4, "wgrad tiling");
+    if (a.P16 == 64) {
+      PST_CHECK_ARG(a.G <= 2, "wgrad tiling (64-pixel units)");
+      const KernT t64[2][2] = {{conv_wgrad_ts_kernel<1, 64, 2>, conv_wgrad_ts_kernel<2, 64, 2>},
+                               {conv_wgrad_ts_kernel<1, 64, 3>, conv_wgrad_ts_kernel<2, 64, 3>}};
+      kern = t64[a.sets == 3 ? 1 : 0][a.G - 1];
+    } else {
+      kern = tab[a.sets == 3 ? 1 : 0][a.P16 == 32 ? 1 : 0][a.G - 1];
+    }
   }
   PST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = a.n_mgroups * a.n_ntiles * a.ksplit;
