@@ -171,8 +171,10 @@ int pst_flush(pst_ctx* ctx);
 int pst_weights(pst_ctx* ctx, uint32_t what, float* out, int64_t cap, int64_t* n);
 
 /* Losses of mini-batches first_mb .. first_mb+n-1 (computed by their forward
- * pass); blocks until available.  Only the context owning the last
- * stage has losses (else PST_E_STATE).  At most the last 1024 are kept. */
+ * pass); waits for the queued work that computes them.  Only the context
+ * owning the last stage has losses (else PST_E_STATE).  At most the last 1024
+ * are kept; asking for a mini-batch whose forward has not been enqueued yet, or
+ * one older than that window, returns PST_E_STATE. */
 int pst_losses(pst_ctx* ctx, int64_t first_mb, int64_t n, float* out);
 
 /* v_s = number of SGD updates applied by each owned stage (local: K values;

@@ -64,6 +64,7 @@ struct pst_ctx {
   int batch = 0;
   // schedule state
   int64_t t = 0, t0 = 0, m0 = 0, n_fed = 0, n_p = INT64_MAX;
+  int64_t n_loss = 0;   // mini-batches whose loss (last stage's forward) has been enqueued
   int mode = MODE_PIPE;
   bool use_graphs = true;
   std::vector<std::map<GraphKey, GraphEntry>> graphs;        // per owned stage
@@ -237,6 +238,7 @@ static void pipe_step(pst_ctx* c) {
   const int K = c->K;
   std::vector<StepPlan> plans(K);
   for (int s = 0; s < K; ++s) plans[s] = plan_step(K, s, c->t, c->t0, c->m0, c->n_fed);
+  if (plans[K - 1].fwd_mb >= 0) c->n_loss = std::max(c->n_loss, plans[K - 1].fwd_mb + 1);
   // all waits first (events of the previous step), then launches, then records
   std::vector<int> active;
   for (int s = 0; s < K; ++s) {
@@ -279,6 +281,7 @@ static void drain(pst_ctx* c) {
 static void np_step(pst_ctx* c) {
   const int K = c->K;
   const int64_t i = c->n_fed - 1;
+  c->n_loss = std::max(c->n_loss, i + 1);
   for (int s = 0; s < K; ++s) {
     if (!c->owns(s)) continue;
     Stage* S = c->stage(s);
@@ -522,6 +525,10 @@ int pst_losses(pst_ctx* c, int64_t first_mb, int64_t n, float* out) {
     Stage* SL = c->stage(c->K - 1);
     if (!SL) throw StateError("losses live on the last stage's rank");
     PST_CHECK_ARG(n <= 1024, "at most 1024 losses are kept");
+    if (first_mb + n > c->n_loss || first_mb < c->n_loss - 1024)
+      throw StateError("losses of mini-batches [" + std::to_string(first_mb) + ", " + std::to_string(first_mb + n) +
+                       ") are not available (computed: [" + std::to_string(std::max<int64_t>(0, c->n_loss - 1024)) +
+                       ", " + std::to_string(c->n_loss) + "))");
     PST_CUDA(cudaSetDevice(SL->dev));
     PST_CUDA(cudaStreamSynchronize(SL->stream));
     SL->read_losses(first_mb, n, out);

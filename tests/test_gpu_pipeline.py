@@ -112,3 +112,44 @@ def test_lenet5_paper_solver_k2(pst):
                                     solver_kw=dict(solver="caffe", lr_policy="inv", inv_gamma=1e-4, inv_power=0.75))
     assert worst[0] <= W_TOL, worst
     assert lerr <= L_TOL, lerr
+
+
+def test_abi_error_behaviour(pst):
+    """include/pst.h's error contract on a live context: invalid arguments return PST_E_INVALID
+    without poisoning the context, losses beyond what was fed / a cap that is too small are
+    reported, and the size query (out = NULL) returns the block size."""
+    import ctypes as C
+    import numpy as np
+    from paper_1912_12675_b200 import binding as Bd
+    L = Bd.lib()
+    net = W.tiny_cnn(hw=8)
+    flat = W.init_params(net, seed=3)
+    with pytest.raises(Bd.PstError) as e:                   # batch out of range
+        pst.Pipeline(net, flat, (), 0, [0.1], 0.1)
+    assert e.value.code == -1
+    with pytest.raises(Bd.PstError):                        # PPV not increasing
+        pst.Pipeline(net, flat, (2, 1), 8, [0.1] * 3, 0.1)
+    n_s, keep = Bd.net_struct(net, flat)                    # solver enum out of range
+    part, keep_p = Bd._partition([], None)
+    lrs = (C.c_float * 1)(0.1)
+    ms = (C.c_int64 * 1)(0)
+    hp = Bd._HParams(8, 0.9, 0.0, C.cast(lrs, C.POINTER(C.c_float)), 0.1, 0, C.cast(ms, C.POINTER(C.c_int64)),
+                     0.1, 1 << 62, 7, 0, 0, 0.0, 0.0)
+    assert L.pst_create(C.byref(n_s), C.byref(part), C.byref(hp), None, C.byref(C.c_void_p())) == -1
+    assert L.pst_create(None, None, None, None, C.byref(C.c_void_p())) == -1
+    pipe = pst.Pipeline(net, flat, (), 8, [0.1], 0.1)
+    x, y = W.make_batch(net.in_shape, 8, 0, seed=1)
+    pipe.step(x, y)
+    n = C.c_int64()
+    assert L.pst_weights(pipe._ctx, 1, None, 0, C.byref(n)) == 0 and n.value == flat.size   # size query
+    small = np.empty(4, dtype=np.float32)
+    rc = L.pst_weights(pipe._ctx, 1, small.ctypes.data_as(C.POINTER(C.c_float)), 4, C.byref(n))
+    assert rc == -1 and n.value == flat.size                # cap too small: INVALID, size reported
+    out = np.empty(4, dtype=np.float32)
+    rc = L.pst_losses(pipe._ctx, 5, 1, out.ctypes.data_as(C.POINTER(C.c_float)))
+    assert rc == -5                                         # mini-batch 5 was never fed: PST_E_STATE
+    assert L.pst_step(pipe._ctx, None) == -1                # null batch
+    pipe.step(x, y)                                         # the context is not poisoned
+    pipe.flush()
+    assert list(pipe.versions()) == [2]
+    pipe.close()
