@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=16, help="images per oracle sample step")
+    p.add_argument("--spin-seconds", type=float, default=1.5, help="untimed spin-up before timing (0 under ncu)")
     return p.parse_args()
 
 
@@ -224,7 +225,7 @@ def main():
     # untimed spin-up: about 1.5 s more of steps so a fresh box's clocks and caches settle (the
     # first bench on a new box otherwise sometimes reads 20-50% slow); the count is agreed on
     # by all ranks, whose stages exchange activations every step
-    n_spin = int(max_over_ranks(float(min(2000, int(1.5 / max(per_step, 1e-4))))))
+    n_spin = int(max_over_ranks(float(min(2000, int(args.spin_seconds / max(per_step, 1e-4))))))
     for i in range(n_spin):
         pipe.step(*dev[(warm + i) % n_pool])
         if i % 50 == 49:
@@ -298,6 +299,14 @@ def main():
                 "hbm_gbs": achieved, "tensor_tflops": tflops,
                 "frac_of_roofline_time": (max(t_bw, t_tc) / (kms / 1e3)) if kms > 0 else None,
                 "peak_source": src}
+    # BASELINE metric's "conv tensor-pipe %": all conv work (fwd + dgrad + wgrad) against the
+    # contraction peak over the conv kernels' own (serially timed) device time
+    conv = [prof[k] for k in ("conv_fwd", "conv_dgrad", "conv_wgrad") if k in prof]
+    conv_ms = sum(v[0] for v in conv)
+    conv_tflops = (sum(v[3] for v in conv) / (conv_ms / 1e3) / 1e12) if conv_ms > 0 else 0.0
+    conv_pipe = {"tflops": conv_tflops, "peak_tflops": tc_peak, "pct": 100.0 * conv_tflops / tc_peak if tc_peak else None,
+                 "conv_ms_per_step": conv_ms / max(1, args.profile_steps),
+                 "note": "sum of conv FLOPs / conv kernel time (per-kernel CUDA events, serial) / " + tc_note}
     kernel_table = {k: {"ms_per_step": v[0] / max(1, args.profile_steps), "launches_per_step": v[1] / max(1, args.profile_steps),
                         "GBps": (v[2] / (v[0] / 1e3) / 1e9) if v[0] > 0 else 0.0,
                         "TFLOPs": (v[3] / (v[0] / 1e3) / 1e12) if v[0] > 0 else 0.0}
@@ -342,7 +351,8 @@ def main():
                        "precision": "fp32 storage, 3xTF32 tensor-core products (" + pst.build_info() + ")",
                        "l2": "inputs larger than L2 (saved-activation ring >> 126 MB)",
                        "lr_per_stage": lr},
-            "clocks": clk, "gpu_launches": launches, "roofline": roofline, "kernels": kernel_table,
+            "clocks": clk, "gpu_launches": launches, "roofline": roofline, "conv_tensor_pipe": conv_pipe,
+            "kernels": kernel_table,
             "e2e": e2e, "cpu_baseline": cpu,
             "paper_context": {"img_s_1gpu_gtx1060": 760, "img_s_2gpu_gtx1060": 1321, "source": "PAPER.md L192"},
         }
