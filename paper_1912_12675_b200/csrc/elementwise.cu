@@ -81,7 +81,10 @@ __global__ void act_to_nchw_kernel(const void* in, int in_f32, float* out, int N
 // ------------------------------------------------------------------ BN forward apply
 // grid (x = pixel chunks of kU*kBlock vectors, y = channel plane): 32-bit pixel indices, the
 // plane's 4 scale/shift pairs in registers, kU independent 16-byte loads in flight per thread.
-constexpr int kU = 4;
+#ifndef PST_KU
+#define PST_KU 4
+#endif
+constexpr int kU = PST_KU;   // 16-byte vectors per thread per pass (plane-blocked kernels)
 __global__ void bn_apply_kernel(const BnApplySpec s) {
   pdl_wait();
   pdl_trigger();
