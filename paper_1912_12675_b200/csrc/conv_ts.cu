@@ -308,7 +308,9 @@ __global__ void __launch_bounds__(kTsThreads, 1)
               ptx::tmem_st16(ta + KC + h * 16, lo + 16 * h);
             }
           }
+          if ((a.knob & 1024) && threadIdx.x == 192) TSL(5, dbg_i[5]++);   // timeline: stores issued
           if (!(a.knob & 512)) ptx::tmem_st_wait();
+          if ((a.knob & 1024) && threadIdx.x == 192) TSL(6, dbg_i[6]++);   // timeline: stores complete
           if (!(a.knob & 256)) ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&afull[my_slot]);
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         if (g == 0) {
           ptx::mbar_wait(&tfull[acc], aph);
           if (!(a.knob & 256)) ptx::tc_fence_after();
-          if (threadIdx.x == 64) TSL(5, dbg_i[5]++);
+          if (threadIdx.x == 64 && !(a.knob & 1024)) TSL(5, dbg_i[5]++);
         }
         float u[16];
         if (a.knob & 64) {
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           warp_chan_sums(s1, s2, lane, wacc + q * 2 * a.BN + 2 * (g * 16 + (lane >> 1)));
         }
       }
-      if (threadIdx.x == 64) TSL(6, dbg_i[6]++);
+      if (threadIdx.x == 64 && !(a.knob & 1024)) TSL(6, dbg_i[6]++);
     }
     if (sums) {
       double* dst = EPI == EPI_BN_STATS ? a.stats : a.bsums;
