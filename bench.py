@@ -187,9 +187,15 @@ def main():
 
     cfg = W.CONFIGS[args.config]
     K = world
-    if K not in cfg.ppv:
+    if K in cfg.ppv:
+        ppv = cfg.ppv[K]
+    elif cfg.net.startswith("resnet"):     # any other stage count: the profile-driven balancer
+        from pst_workloads import balance as Bl
+        netspec = cfg.netspec()
+        ppv = Bl.balance_ppv(Bl.resnet_layer_costs(netspec, Bl.load_cost_table()), K,
+                             Bl.resnet_boundaries(netspec))
+    else:
         raise SystemExit(f"no PPV for {K} stages in config {cfg.name}")
-    ppv = cfg.ppv[K]
     B = args.batch or cfg.batch
     net = cfg.netspec()
     params = W.init_params(net, seed=42)
