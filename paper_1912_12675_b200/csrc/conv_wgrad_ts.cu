@@ -361,6 +361,9 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   a.n_units = ceil_div(N, a.nb) * a.ny;
   const int base = a.n_mgroups * a.n_ntiles;
   a.ksplit = std::max(1, std::min(std::max(1, a.n_units / 2), num_sm / base));
+  // cap on the split (PST_WT_KSPLIT_MAX experiments): fewer fp32 partials to write and reduce
+  static const int ks_max = [] { const char* e = std::getenv("PST_WT_KSPLIT_MAX"); return e ? std::atoi(e) : 0; }();
+  if (ks_max > 0) a.ksplit = std::min(a.ksplit, ks_max);
   if (out) *reinterpret_cast<WtArgs*>(out) = a;
   return true;
 }
