@@ -364,6 +364,8 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   // cap on the split (PST_WT_KSPLIT_MAX experiments): fewer fp32 partials to write and reduce
   static const int ks_max = [] { const char* e = std::getenv("PST_WT_KSPLIT_MAX"); return e ? std::atoi(e) : 0; }();
   if (ks_max > 0) a.ksplit = std::min(a.ksplit, ks_max);
+  static const int ks_big = [] { const char* e = std::getenv("PST_WT_KSPLIT_MAX_BIG"); return e ? std::atoi(e) : 0; }();
+  if (ks_big > 0 && a.rows > 256) a.ksplit = std::min(a.ksplit, ks_big);   // the many-row (64-channel) layers only
   if (out) *reinterpret_cast<WtArgs*>(out) = a;
   return true;
 }
