@@ -207,6 +207,16 @@ int pst_profile(pst_ctx* ctx, int32_t enable);
 int pst_profile_read(pst_ctx* ctx, int32_t cls, double* ms, int64_t* launches, double* bytes,
                      double* flops);
 
+/* Per-stage timing (balance diagnostics for the partition, SURVEY f-1).  enable != 0: from the
+ * next pst_step on, the owned stages of each step run one after another (stage s waits for
+ * stage s-1's work of the same step; the schedule's results are unchanged) with a CUDA-event
+ * pair around each stage's step program, so each stage's device time is measured alone.
+ * Counters are reset.  enable == 0: back to concurrent stages. */
+int pst_stage_timing(pst_ctx* ctx, int32_t enable);
+/* Accumulated milliseconds per owned stage since pst_stage_timing(ctx, 1) (cap entries) and
+ * the number of timed steps.  Synchronises. */
+int pst_stage_times(pst_ctx* ctx, double* ms, int32_t cap, int64_t* steps);
+
 void pst_destroy(pst_ctx* ctx);
 const char* pst_last_error(const pst_ctx* ctx);
 

@@ -93,6 +93,8 @@ def lib():
         "pst_build_info": (C.c_char_p, []),
         "pst_launches": (C.c_int, [C.c_void_p, P(C.c_int64)]),
         "pst_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+        "pst_stage_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+        "pst_stage_times": (C.c_int, [C.c_void_p, P(C.c_double), C.c_int32, P(C.c_int64)]),
         "pst_profile_read": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_double), P(C.c_int64), P(C.c_double),
                                        P(C.c_double)]),
         "pst_op_conv2d_fwd": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 8),
@@ -280,6 +282,18 @@ class Pipeline:
 
     def profile(self, enable: bool):
         self._c(lib().pst_profile(self._ctx, 1 if enable else 0))
+
+    def stage_timing(self, enable: bool):
+        """Serialise the stages within each step and time each one (pst_stage_timing)."""
+        self._c(lib().pst_stage_timing(self._ctx, 1 if enable else 0))
+
+    def stage_times(self):
+        """(ms per owned stage accumulated since stage_timing(True), timed steps)."""
+        n = self.K if self.rank is None else 1
+        ms = (C.c_double * n)()
+        steps = C.c_int64()
+        self._c(lib().pst_stage_times(self._ctx, ms, n, C.byref(steps)))
+        return np.array(ms[:n]), steps.value
 
     KERNEL_CLASSES = ("conv_fwd", "conv_dgrad", "conv_wgrad", "bn_apply", "bwd_pre", "bn_bwd", "pool", "sgd",
                       "loss", "misc")

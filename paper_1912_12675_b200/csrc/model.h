@@ -57,6 +57,12 @@ std::vector<std::pair<int, int>> partition(const NetInfo& net, int K, const int3
 struct StepPlan { int64_t bwd_mb = -1, fwd_mb = -1; };
 StepPlan plan_step(int K, int s, int64_t t, int64_t t0, int64_t m0, int64_t n_fed);
 
-inline int ring_slots(int K, int s) { return 2 * (K - s) + 1; }
+// Saved-activation / input ring slots per stage.  A stage needs 2(K-s)-1 slots for the paper's
+// activation storage plus 2 so a forward never overwrites a slot an in-flight copy
+// still reads; every stage uses the same even size 2K+2 >= 2(K-s)+1, so all ring indices and the
+// gradient-buffer parity cycle with ONE period and a stage needs at most 2K+2 distinct step graphs
+// (with per-stage sizes 2(K-s)+1 the graph key cycles with lcm(2, R_s-1, R_s, R_s+1): 6630 step
+// graphs for the second stage of an 8-stage pipeline).
+inline int ring_slots(int K, int s) { (void)s; return 2 * K + 2; }
 
 }  // namespace pst

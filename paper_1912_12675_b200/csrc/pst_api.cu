@@ -65,6 +65,12 @@ struct pst_ctx {
   // schedule state
   int64_t t = 0, t0 = 0, m0 = 0, n_fed = 0, n_p = INT64_MAX;
   int64_t n_loss = 0;   // mini-batches whose loss (last stage's forward) has been enqueued
+  // per-stage timing (pst_stage_timing): stages serialised within a step, events around each
+  bool stage_timing = false;
+  std::vector<cudaEvent_t> st_beg, st_end;      // per owned stage
+  std::vector<double> st_ms;
+  int64_t st_steps = 0;
+  bool st_pending = false;
   int mode = MODE_PIPE;
   bool use_graphs = true;
   std::vector<std::map<GraphKey, GraphEntry>> graphs;        // per owned stage
@@ -258,7 +264,27 @@ static void pipe_step(pst_ctx* c) {
              s > 0 && prev.fwd_mb >= 0 ? slot(prev.fwd_mb, S->R) : -1,
              s < K - 1 && next.bwd_mb >= 0 ? (next.bwd_mb & 1) : -1};
     if (p.bwd_mb < 0 && p.fwd_mb < 0 && key.k[5] < 0 && key.k[6] < 0) continue;
+    const int li = c->local_index(s);
+    if (c->stage_timing) {
+      if (!c->dist && s > 0) PST_CUDA(cudaStreamWaitEvent(S->stream, c->st_end[s - 1], 0));
+      PST_CUDA(cudaEventRecord(c->st_beg[li], S->stream));
+    }
     run_program(c, s, key, [&](cudaStream_t st) { enqueue_pipe(c, s, p, prev, next, st); });
+    if (c->stage_timing) PST_CUDA(cudaEventRecord(c->st_end[li], S->stream));
+  }
+  if (c->stage_timing) {   // accumulate this step's per-stage times (diagnostic: synchronises)
+    for (int s = 0; s < K; ++s) {
+      if (!c->owns(s)) continue;
+      const int li = c->local_index(s);
+      PST_CUDA(cudaEventSynchronize(c->st_end[li]));
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, c->st_beg[li], c->st_end[li]) == cudaSuccess) c->st_ms[li] += ms;
+      cudaGetLastError();
+      // a stage with no work this step leaves its events at the previous step: re-record both
+      PST_CUDA(cudaEventRecord(c->st_beg[li], c->stage(s)->stream));
+      PST_CUDA(cudaEventRecord(c->st_end[li], c->stage(s)->stream));
+    }
+    c->st_steps += 1;
   }
   for (int s = 0; s < K; ++s) {
     if (!c->owns(s)) continue;
@@ -646,6 +672,38 @@ int pst_profile(pst_ctx* c, int32_t enable) {
     sync_all(c);
     prof::read(-1, nullptr, nullptr, nullptr, nullptr);
     prof::enabled = enable != 0;
+  });
+}
+
+int pst_stage_timing(pst_ctx* c, int32_t enable) {
+  if (!c) return PST_E_INVALID;
+  return guard(c, [&] {
+    sync_all(c);
+    if (c->st_beg.empty()) {
+      for (size_t i = 0; i < c->stages.size(); ++i) {
+        PST_CUDA(cudaSetDevice(c->stages[i]->dev));
+        cudaEvent_t a, b;
+        PST_CUDA(cudaEventCreate(&a));
+        PST_CUDA(cudaEventCreate(&b));
+        PST_CUDA(cudaEventRecord(a, c->stages[i]->stream));
+        PST_CUDA(cudaEventRecord(b, c->stages[i]->stream));
+        c->st_beg.push_back(a);
+        c->st_end.push_back(b);
+      }
+    }
+    c->st_ms.assign(c->stages.size(), 0.0);
+    c->st_steps = 0;
+    c->stage_timing = enable != 0;
+  });
+}
+
+int pst_stage_times(pst_ctx* c, double* ms, int32_t cap, int64_t* steps) {
+  if (!c || !ms) return PST_E_INVALID;
+  return guard(c, [&] {
+    PST_CHECK_ARG(cap >= (int32_t)c->stages.size(), "cap");
+    sync_all(c);
+    for (size_t i = 0; i < c->stages.size(); ++i) ms[i] = i < c->st_ms.size() ? c->st_ms[i] : 0.0;
+    if (steps) *steps = c->st_steps;
   });
 }
 
