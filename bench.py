@@ -58,6 +58,25 @@ def dist_env():
     return rank, world, local
 
 
+def spawn_ranks(n):
+    """`python bench.py --gpus N` without a launcher: start N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1 and return their exit code (rank 0 prints the line)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def share_gpu():
+    """PST_BENCH_SHARE_GPU=1: every rank on cuda:0 (a functional check of the N-rank path on a one-GPU
+    box; NCCL needs a distinct NCCL_HOSTID per rank to accept two ranks on one device and then uses
+    its socket transport).  Numbers from such a run are not throughput measurements."""
+    return os.environ.get("PST_BENCH_SHARE_GPU") == "1"
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -145,10 +164,11 @@ def run_reference(args, rank, world):
     rate = args.steps * sample / tot
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "img/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps * (B / sample),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.net}_cifar10_b{B}", "model": cfg.net, "global_batch": B,
-                   "stages": 1, "parallelism": "none (CPU oracle)"},
+        "config": {"workload": f"{cfg.net}_cifar10_b{B}_pp{world}", "model": cfg.net, "global_batch": B,
+                   "stages": world, "parallelism": "none (CPU oracle on the host, rank 0 only)",
+                   "sample": f"{sample} of the {B} images per step"},
         "cpu_baseline": {"value": rate, "unit": "img/s", "cores": blas_threads(), "kind": "oracle",
                          "sample": f"1 non-pipelined SGD step of {cfg.net} on a {sample}-image slice per step"},
         "e2e": {"value": rate, "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -160,6 +180,10 @@ def run_reference(args, rank, world):
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -167,6 +191,13 @@ def main():
     import pst_workloads as W
     import paper_1912_12675_b200 as pst
 
+    shared = share_gpu() and world > 1
+    if shared:
+        local = 0
+        os.environ["NCCL_HOSTID"] = f"pst-bench-rank{rank}"
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+    elif torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
@@ -205,7 +236,8 @@ def main():
     if world > 1:
         nid = [pst.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(nid, src=0)
-        pipe = pst.Pipeline(net, params, ppv, B, lr, cfg.base_lr, devices=list(range(K)), rank=rank,
+        pipe = pst.Pipeline(net, params, ppv, B, lr, cfg.base_lr, devices=[0] * K if shared else list(range(K)),
+                            rank=rank,
                             nccl_id=nid[0], **kw)
         my_stage = rank
     else:
@@ -349,7 +381,7 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "img/s", "n_gpus": world, "steps": args.steps,
-            "warmup": warm, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "warmup_steps_run": warm, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": (value / PAPER_IMG_S[world]) if world in PAPER_IMG_S else None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{cfg.net}_cifar10_b{B}_pp{K}", "model": cfg.net, "global_batch": B,

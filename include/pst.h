@@ -34,8 +34,7 @@
  *
  * Ownership: the library copies every input structure and array at create
  * time; the caller keeps ownership of all buffers it passes.  pst_step has
- * finished reading the host batch when it returns (device batches must stay
- * valid until the next pst_* call on this context).  Output buffers are
+ * finished reading a host batch when it returns (device batches: see pst_batch).  Output buffers are
  * caller-allocated; pass out == NULL to query the required size in *n.
  *
  * Threading: one host thread of control per context.
@@ -138,12 +137,18 @@ typedef struct {
 
 /* One mini-batch.  x: NCHW float32 [batch][in_c][in_h][in_w]; y: int32 [batch]
  * labels in [0, n_classes).  on_device != 0: both are device pointers on stage
- * 0's / stage K-1's device.  In distributed mode only rank 0 reads x and only
- * rank K-1 reads y (others may pass NULL). */
+ * 0's / stage K-1's device, produced by work on `stream` (a cudaStream_t; NULL =
+ * the legacy default stream): pst_step orders its copies after everything
+ * enqueued on that stream so far.  In distributed mode only rank 0 reads x and
+ * only rank K-1 reads y (others may pass NULL).
+ * Lifetime: a host batch may be reused as soon as pst_step returns; a device
+ * batch must stay valid (unmodified) until the NEXT pst_step, pst_flush or
+ * pst_sync call on this context returns. */
 typedef struct {
   const float* x;
   const int32_t* y;
   int32_t on_device;
+  void* stream;
 } pst_batch;
 
 /* what-flags for pst_weights; blocks are concatenated in this order. */
@@ -216,6 +221,16 @@ int pst_stage_timing(pst_ctx* ctx, int32_t enable);
 /* Accumulated milliseconds per owned stage since pst_stage_timing(ctx, 1) (cap entries) and
  * the number of timed steps.  Synchronises. */
 int pst_stage_times(pst_ctx* ctx, double* ms, int32_t cap, int64_t* steps);
+
+/* Device memory of an owned stage (the paper's memory analysis, section 3 and Table 6
+ * P:L198-212 section 6.6: a stage keeps the activations of 2(K-s)-1 mini-batches).  out[cap >= 5]:
+ *   out[0] device bytes the stage allocated (all buffers);
+ *   out[1] saved-activation ring slots R_s this build keeps (2(K-s)+1 rounded up to a divisor of
+ *          2K+2, model.h ring_slots);
+ *   out[2] the paper's count 2(K-s)-1;
+ *   out[3] bytes of the saved forward state of one mini-batch (one slot);
+ *   out[4] bytes of the stage's parameters (one float32 copy). */
+int pst_memory(pst_ctx* ctx, int32_t stage, int64_t* out, int32_t cap);
 
 void pst_destroy(pst_ctx* ctx);
 const char* pst_last_error(const pst_ctx* ctx);

@@ -56,7 +56,7 @@ class _Dist(C.Structure):
 
 
 class _Batch(C.Structure):
-    _fields_ = [("x", C.c_void_p), ("y", C.c_void_p), ("on_device", C.c_int32)]
+    _fields_ = [("x", C.c_void_p), ("y", C.c_void_p), ("on_device", C.c_int32), ("stream", C.c_void_p)]
 
 
 _lib = None
@@ -84,6 +84,7 @@ def lib():
         "pst_stream": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_void_p)]),
         "pst_sync": (C.c_int, [C.c_void_p]),
         "pst_destroy": (None, [C.c_void_p]),
+        "pst_memory": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_int64), C.c_int32]),
         "pst_last_error": (C.c_char_p, [C.c_void_p]),
         "pst_nccl_unique_id": (C.c_int, [C.c_void_p]),
         "pst_partition_ranges": (C.c_int, [P(_Net), P(_Partition), P(C.c_int32)]),
@@ -225,10 +226,13 @@ class Pipeline:
     def step(self, x, y):
         """x: float32 NCHW, y: int32 labels; numpy (host) arrays or torch CUDA tensors."""
         b = _Batch()
-        if hasattr(x, "data_ptr"):
+        t = x if hasattr(x, "data_ptr") else y
+        if hasattr(t, "data_ptr"):
+            import torch
             b.x = x.data_ptr() if x is not None else None
             b.y = y.data_ptr() if y is not None else None
             b.on_device = 1
+            b.stream = torch.cuda.current_stream(t.device).cuda_stream   # the producer stream
         else:
             xs = np.ascontiguousarray(x, dtype=np.float32) if x is not None else None
             ys = np.ascontiguousarray(y, dtype=np.int32) if y is not None else None
@@ -274,6 +278,13 @@ class Pipeline:
 
     def sync(self):
         self._c(lib().pst_sync(self._ctx))
+
+    def memory(self, stage: int) -> dict:
+        """Device memory of an owned stage (pst_memory)."""
+        out = (C.c_int64 * 5)()
+        self._c(lib().pst_memory(self._ctx, stage, out, 5))
+        return {"bytes_total": out[0], "ring_slots": out[1], "paper_slots": out[2], "bytes_per_slot": out[3],
+                "param_bytes": out[4]}
 
     def launches(self) -> int:
         n = C.c_int64()

@@ -80,6 +80,7 @@ struct pst_ctx {
   int32_t* pin_y[2] = {nullptr, nullptr};
   cudaEvent_t pin_ev[2] = {nullptr, nullptr};
   cudaEvent_t pin_ev2[2] = {nullptr, nullptr};
+  cudaEvent_t prod_ev = nullptr;   // recorded on a device batch's producer stream
   int pin_i = 0;
 
   Stage* stage(int s) {
@@ -440,6 +441,8 @@ int pst_create(const pst_net* net, const pst_partition* part, const pst_hparams*
       PST_CUDA(cudaEventCreateWithFlags(&c->pin_ev[i], cudaEventDisableTiming));
       PST_CUDA(cudaEventCreateWithFlags(&c->pin_ev2[i], cudaEventDisableTiming));
     }
+    PST_CUDA(cudaSetDevice(c->stages[0]->dev));
+    PST_CUDA(cudaEventCreateWithFlags(&c->prod_ev, cudaEventDisableTiming));
   });
   if (rc != PST_OK) {
     g_last_global_error = c->err.empty() ? g_last_global_error : c->err;
@@ -465,10 +468,19 @@ int pst_step(pst_ctx* c, const pst_batch* batch) {
     c->pin_i ^= 1;
     Stage* S0 = c->stage(0);
     Stage* SL = c->stage(c->K - 1);
-    (void)pi;
-    // the pinned slot is reusable once the copies issued two steps ago have executed
-    PST_CUDA(cudaEventSynchronize(c->pin_ev[pi]));
-    PST_CUDA(cudaEventSynchronize(c->pin_ev2[pi]));
+    // The previous step's batch copies must have executed before this call returns (pst_batch
+    // lifetime: a device batch stays valid until the next pst_step/pst_flush/pst_sync) and before
+    // the pinned slot of two steps ago is reused.  The copy of step t-1 sits on the stage stream
+    // behind step t-2's work, so the host runs at most one step ahead of the device.
+    PST_CUDA(cudaEventSynchronize(c->pin_ev[pi ^ 1]));
+    PST_CUDA(cudaEventSynchronize(c->pin_ev2[pi ^ 1]));
+    if (batch->on_device) {   // order the copies after the producer's work (pst_batch.stream)
+      cudaStream_t prod = batch->stream ? (cudaStream_t)batch->stream : cudaStreamLegacy;
+      PST_CUDA(cudaSetDevice(c->stages[0]->dev));   // prod_ev lives on the first owned stage's device
+      PST_CUDA(cudaEventRecord(c->prod_ev, prod));
+      for (Stage* S : {S0, SL})
+        if (S) PST_CUDA(cudaStreamWaitEvent(S->stream, c->prod_ev, 0));
+    }
     if (S0) {
       PST_CHECK_ARG(batch->x != nullptr, "batch x is null");
       PST_CUDA(cudaSetDevice(S0->dev));
@@ -605,6 +617,9 @@ void pst_destroy(pst_ctx* c) {
     if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
     if (c->pin_ev2[i]) cudaEventDestroy(c->pin_ev2[i]);
   }
+  if (c->prod_ev) cudaEventDestroy(c->prod_ev);
+  for (auto e : c->st_beg) cudaEventDestroy(e);
+  for (auto e : c->st_end) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
   c->stages.clear();
   delete c;
@@ -713,6 +728,20 @@ int pst_profile_read(pst_ctx* c, int32_t cls, double* ms, int64_t* launches, dou
     PST_CHECK_ARG(cls >= 0 && cls < prof::NCLS, "kernel class");
     sync_all(c);
     prof::read(cls, ms, launches, bytes, flops);
+  });
+}
+
+int pst_memory(pst_ctx* c, int32_t stage, int64_t* out, int32_t cap) {
+  if (!c || !out) return PST_E_INVALID;
+  return guard(c, [&] {
+    PST_CHECK_ARG(stage >= 0 && stage < c->K && c->owns(stage), "stage not owned by this context");
+    PST_CHECK_ARG(cap >= 5, "cap");
+    Stage* S = c->stage(stage);
+    out[0] = (int64_t)S->bytes_total;
+    out[1] = S->R;
+    out[2] = 2 * (c->K - stage) - 1;
+    out[3] = (int64_t)S->bytes_slot;
+    out[4] = S->n_params * (int64_t)sizeof(float);
   });
 }
 

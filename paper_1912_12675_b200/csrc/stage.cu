@@ -28,6 +28,7 @@ T* Stage::alloc(size_t n, bool zero) {
   cudaError_t e = cudaMalloc(&p, n * sizeof(T));
   if (e != cudaSuccess) throw CudaError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
   allocs_.push_back(p);
+  bytes_total += n * sizeof(T);
   if (zero) PST_CUDA(cudaMemset(p, 0, n * sizeof(T)));
   return static_cast<T*>(p);
 }
@@ -51,6 +52,7 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
   // input ring of the stage
   const LayerInfo& f0 = net.layers[l0];
   for (int r = 0; r < R; ++r) xin_.push_back(alloc<act_t>((size_t)B * f0.in_H * f0.in_W * f0.in_Cp));
+  bytes_slot += (size_t)B * f0.in_H * f0.in_W * f0.in_Cp * sizeof(act_t);
   if (is_first()) xstage_ = alloc<float>((size_t)B * net.in_C * net.in_H * net.in_W);
 
   // per-layer buffers
@@ -81,6 +83,7 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     LayerBufs& b = L_[l - l0];
     const size_t out_el = (size_t)B * li.Ho * li.Wo * li.Coutp;
     const bool last_net = (l == (int)net.layers.size() - 1);
+    const size_t before_ring = bytes_total;
     for (int r = 0; r < R; ++r) {
       if (li.spec.bn) b.y.push_back(alloc<act_t>(out_el, false));
       if (last_net) b.zf.push_back(alloc<float>(out_el));
@@ -93,6 +96,7 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
       }
       if (li.spec.bn) b.saved.push_back(alloc<float>(2 * li.Coutp));
     }
+    bytes_slot += (bytes_total - before_ring) / R;
     b.gpre = alloc<act_t>(out_el, false);
     if (li.spec.bn) b.gy = alloc<act_t>(out_el, false);
     const bool need_gin = !(is_first() && l == l0);

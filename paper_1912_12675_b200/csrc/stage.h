@@ -61,6 +61,8 @@ class Stage {
 
   const int s, K, l0, l1, dev, R, batch_;
   int64_t p_base = 0, n_params = 0;
+  size_t bytes_total = 0;   // device bytes this stage allocated
+  size_t bytes_slot = 0;    // saved forward state of ONE mini-batch (input + per-layer y/z/pool/argmax/stats)
   cudaStream_t stream = nullptr;
   // weight-gradient side stream: wgrad(l) depends only on dY(l) and the saved input, so it runs
   // concurrently with the dgrad chain of the layers below and joins before the update

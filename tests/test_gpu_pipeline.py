@@ -30,37 +30,29 @@ def pst():
 @pytest.mark.parametrize("K,ppv", [(1, ()), (2, (3,)), (3, (1, 3))])
 def test_tiny_resnet_pipeline(pst, K, ppv):
     net = W.tiny_resnet(width=16, hw=8, n=1)
-    worst, lerr, vers, _ = run_both(pst, net, ppv, 32, 8, [0.05] * (K - 1) + [0.1])
-    assert worst[0] <= W_TOL, worst
-    assert lerr <= L_TOL, lerr
-    assert list(vers) == [8] * K
+    P = run_both(pst, net, ppv, 32, 8, [0.05] * (K - 1) + [0.1]).assert_ok()
+    assert list(P.versions) == [8] * K
 
 
 @pytest.mark.parametrize("K,ppv", [(1, ()), (2, (2,)), (4, (1, 2, 3))])
 def test_tiny_cnn_pipeline(pst, K, ppv):
     net = W.tiny_cnn(hw=8)
-    worst, lerr, vers, _ = run_both(pst, net, ppv, 32, 8, [0.05] * K, wd=5e-4)
-    assert worst[0] <= W_TOL, worst
-    assert lerr <= L_TOL, lerr
+    run_both(pst, net, ppv, 32, 8, [0.05] * K, wd=5e-4).assert_ok()
 
 
 def test_lenet5_config1_k2(pst):
     """BASELINE.json configs[0]: LeNet-5, MNIST-shaped, batch 64, 2 stages, 20 steps."""
     cfg = W.CONFIGS["lenet5"]
-    worst, lerr, vers, _ = run_both(pst, W.lenet5(), cfg.ppv[2], 64, 20, cfg.lr_vector(2), mom=cfg.momentum,
-                                    wd=cfg.weight_decay)
-    assert worst[0] <= W_TOL, worst
-    assert lerr <= L_TOL, lerr
+    run_both(pst, W.lenet5(), cfg.ppv[2], 64, 20, cfg.lr_vector(2), mom=cfg.momentum,
+             wd=cfg.weight_decay).assert_ok()
 
 
 def test_hybrid_switch(pst):
     """pipelined for n_p mini-batches, drain, then non-pipelined (AMB-10)."""
     net = W.tiny_resnet(width=16, hw=8, n=1)
-    worst, lerr, vers, ref = run_both(pst, net, (1, 3), 32, 9, [0.02, 0.05, 0.1], lr_np=0.08, n_p=4, spe=2,
-                                      milestones=(3,))
-    assert worst[0] <= W_TOL, worst
-    assert lerr <= L_TOL, lerr
-    assert list(vers) == [9, 9, 9]
+    P = run_both(pst, net, (1, 3), 32, 9, [0.02, 0.05, 0.1], lr_np=0.08, n_p=4, spe=2,
+                 milestones=(3,)).assert_ok()
+    assert list(P.versions) == [9, 9, 9]
 
 
 def test_distributed_mode_single_rank(pst):
@@ -97,21 +89,15 @@ def test_solver_variants(pst, skw, ppv):
     mid-run so the Caffe form (lr folded into the history) differs from the PyTorch form."""
     net = W.tiny_cnn(hw=8)
     K = len(ppv) + 1
-    worst, lerr, vers, _ = run_both(pst, net, ppv, 32, 10, [0.05] * K, wd=5e-4, milestones=(2,), spe=3,
-                                    solver_kw=skw)
-    assert worst[0] <= W_TOL, worst
-    assert lerr <= L_TOL, lerr
+    run_both(pst, net, ppv, 32, 10, [0.05] * K, wd=5e-4, milestones=(2,), spe=3, solver_kw=skw).assert_ok()
 
 
 def test_lenet5_paper_solver_k2(pst):
     """configs[0] with the paper's own LeNet-5 solver: Caffe SGD, momentum 0.9, wd 5e-4, lr 0.01
     with the "inv" policy (L284; gamma 1e-4 / power 0.75, Caffe's LeNet values, external), 2 stages."""
     cfg = W.CONFIGS["lenet5"]
-    worst, lerr, vers, _ = run_both(pst, W.lenet5(), cfg.ppv[2], 64, 20, cfg.lr_vector(2), mom=cfg.momentum,
-                                    wd=cfg.weight_decay,
-                                    solver_kw=dict(solver="caffe", lr_policy="inv", inv_gamma=1e-4, inv_power=0.75))
-    assert worst[0] <= W_TOL, worst
-    assert lerr <= L_TOL, lerr
+    run_both(pst, W.lenet5(), cfg.ppv[2], 64, 20, cfg.lr_vector(2), mom=cfg.momentum, wd=cfg.weight_decay,
+             solver_kw=dict(solver="caffe", lr_policy="inv", inv_gamma=1e-4, inv_power=0.75)).assert_ok()
 
 
 def test_abi_error_behaviour(pst):

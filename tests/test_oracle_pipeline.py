@@ -157,27 +157,50 @@ def half_square(y, _label):
     return 0.5 * float(y * y), y
 
 
-def test_scalar_worked_example_golden():
-    gold = json.load(open(os.path.join(GOLDEN, "scalar_pipeline_k2.json")))
+@pytest.mark.parametrize("name", ["scalar_pipeline_k2.json", "scalar_pipeline_k3_momentum.json"])
+def test_scalar_worked_example_golden(name):
+    """Oracle A and Oracle B against the closed-form scalar recursion of tools/make_golden_scalar.py
+    (written from P:L61-L75 without importing oracle/); the K=2 file reproduces SURVEY Appendix B's
+    hand-derived table to its 8 printed decimals, the K=3 file adds momentum and weight decay."""
+    gold = json.load(open(os.path.join(GOLDEN, name)))
     atol = gold["atol"]
+    K = gold["hparams"]["K"]
     N = len(gold["pipelined"]["loss"])
     data = [(1.0, None)] * N
-    hp = Pl.HParams(lr_pipelined=[0.1, 0.1], lr_nonpipelined=0.1, momentum=0.0, weight_decay=0.0)
-    p0 = [[{"W": np.float64(1.0)}], [{"W": np.float64(1.0)}]]
-    rb = Pl.run_clocked([ScalarStage(), ScalarStage()], p0, data, hp, loss_fn=half_square)
+    lr, mu, wd = gold["hparams"]["lr"], gold["hparams"]["momentum"], gold["hparams"]["weight_decay"]
+    hp = Pl.HParams(lr_pipelined=[lr] * K, lr_nonpipelined=lr, momentum=mu, weight_decay=wd)
+    p0 = [[{"W": np.float64(1.0)}] for _ in range(K)]
+    stages = lambda: [ScalarStage() for _ in range(K)]
+    rb = Pl.run_clocked(stages(), p0, data, hp, loss_fn=half_square)
     np.testing.assert_allclose(rb.losses, gold["pipelined"]["loss"], atol=atol, rtol=0)
     # per-mini-batch weights after each update: Oracle A's history
-    a_after, b_after = [], []
     for n in range(1, N + 1):
-        ra = Pl.run_versioned([ScalarStage(), ScalarStage()], p0, data[:n], hp, loss_fn=half_square)
-        a_after.append(float(ra.params[0][0]["W"]))
-        b_after.append(float(ra.params[1][0]["W"]))
-    np.testing.assert_allclose(a_after, gold["pipelined"]["a_after"], atol=atol, rtol=0)
-    np.testing.assert_allclose(b_after, gold["pipelined"]["b_after"], atol=atol, rtol=0)
-    # non-pipelined (K=1 over the two-layer net == hybrid with n_p = 0)
-    rn = Pl.run_clocked([ScalarStage(), ScalarStage()], p0, data, hp, loss_fn=half_square, n_p=0)
+        ra = Pl.run_versioned(stages(), p0, data[:n], hp, loss_fn=half_square)
+        got = [float(ra.params[s][0]["W"]) for s in range(K)]
+        np.testing.assert_allclose(got, [gold["pipelined"]["w_after"][s][n - 1] for s in range(K)], atol=atol, rtol=0)
+    # non-pipelined (K=1 over the chain == hybrid with n_p = 0)
+    rn = Pl.run_clocked(stages(), p0, data, hp, loss_fn=half_square, n_p=0)
     np.testing.assert_allclose(rn.losses, gold["nonpipelined"]["loss"], atol=atol, rtol=0)
-    assert abs(float(rn.params[0][0]["W"]) - gold["nonpipelined"]["a_after"][-1]) < atol
+    np.testing.assert_allclose([float(rn.params[s][0]["W"]) for s in range(K)],
+                               [gold["nonpipelined"]["w_after"][s][-1] for s in range(K)], atol=atol, rtol=0)
+
+
+def test_golden_files_match_their_generator():
+    """The committed golden files are exactly what tools/make_golden_scalar.py writes today, and the
+    K=2 file agrees with SURVEY Appendix B's hand-derived 8-decimal table."""
+    import subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "make_golden_scalar.py"), "--check"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    gold = json.load(open(os.path.join(GOLDEN, "scalar_pipeline_k2.json")))
+    hand = {"loss": [0.5, 0.405, 0.32805, 0.21523361, 0.15053029],
+            "a": [0.9, 0.819, 0.75339, 0.70556031, 0.66880078], "b": [0.9, 0.81, 0.729, 0.669951, 0.6250133],
+            "np_loss": [0.5, 0.32805, 0.23399258, 0.17623916, 0.13796786]}
+    np.testing.assert_allclose(gold["pipelined"]["loss"], hand["loss"], atol=5e-9)
+    np.testing.assert_allclose(gold["pipelined"]["w_after"][0], hand["a"], atol=5e-9)
+    np.testing.assert_allclose(gold["pipelined"]["w_after"][1], hand["b"], atol=5e-9)
+    np.testing.assert_allclose(gold["nonpipelined"]["loss"], hand["np_loss"], atol=5e-9)
 
 
 @pytest.mark.parametrize("n_p", [0, 1, 3, 7])

@@ -67,3 +67,58 @@ def test_inv_policy_closed_form():
     assert Pl.learning_rate(hp, 0, 0) == pytest.approx(0.01)
     assert Pl.learning_rate(hp, 0, 10000) == pytest.approx(0.01 * 2 ** -0.75)
     assert Pl.learning_rate(hp, 0, 30000) == pytest.approx(0.01 * 4 ** -0.75)
+
+
+def test_caffe_form_two_steps_changing_lr_by_hand():
+    """Caffe's documented update (V <- mu V + alpha (g + lambda W); W <- W - V; Nesterov:
+    W <- W - ((1 + mu) V_new - mu V_old)) with the rate changing between steps, worked by hand:
+    w0 = 1, g = 0.5 then 0.25, mu = 0.9, lambda = 0.1, alpha = 0.1 then 0.01.
+      step 1: g' = 0.5 + 0.1*1 = 0.6;          V1 = 0.06;   w1 = 0.94       (Nesterov: 1 - 1.9*0.06 = 0.886)
+      step 2: g' = 0.25 + 0.1*0.94 = 0.344;    V2 = 0.054 + 0.00344 = 0.05744;  w2 = 0.88256
+              Nesterov: g' = 0.25 + 0.0886 = 0.3386; V2 = 0.054 + 0.003386 = 0.057386;
+                        w2 = 0.886 - (1.9*0.057386 - 0.9*0.06) = 0.8309666"""
+    w, V = Lx.sgd_caffe(np.float64(1.0), np.float64(0.0), 0.5, 0.1, 0.9, 0.1)
+    assert (w, V) == pytest.approx((0.94, 0.06), abs=1e-15)
+    w, V = Lx.sgd_caffe(w, V, 0.25, 0.01, 0.9, 0.1)
+    assert (w, V) == pytest.approx((0.88256, 0.05744), abs=1e-15)
+    w, V = Lx.sgd_caffe(np.float64(1.0), np.float64(0.0), 0.5, 0.1, 0.9, 0.1, nesterov=True)
+    assert (w, V) == pytest.approx((0.886, 0.06), abs=1e-15)
+    w, V = Lx.sgd_caffe(w, V, 0.25, 0.01, 0.9, 0.1, nesterov=True)
+    assert (w, V) == pytest.approx((0.8309666, 0.057386), abs=1e-15)
+
+
+@pytest.mark.parametrize("spe,milestones,gamma,n_p", [(3, (2, 4), 0.1, None), (1, (1, 3, 5), 0.5, None),
+                                                       (4, (2,), 0.2, 12), (2, (1, 6), 0.1, 6)])
+def test_learning_rate_matches_torch_multisteplr(spe, milestones, gamma, n_p):
+    """oracle.pipeline.learning_rate (reading AMB-8: the rate of the update from mini-batch i is the
+    stage's base rate x gamma^(#milestones <= epoch(i)), epoch(i) = i // steps_per_epoch; after the
+    hybrid switch at n_p every stage uses the non-pipelined base, reading AMB-10)
+    against torch.optim.lr_scheduler.MultiStepLR stepped once per epoch, one optimizer per stage.
+    At the switch the schedule restarts from the non-pipelined base as a user would: a fresh
+    optimizer + MultiStepLR fast-forwarded to the switch epoch."""
+    lrs = [0.001, 0.02, 0.1]
+    lr_np = 0.05
+    hp = Pl.HParams(lr_pipelined=lrs, lr_nonpipelined=lr_np, milestones=milestones, gamma=gamma,
+                    steps_per_epoch=spe)
+    N = 30
+
+    def make(base, epochs_done=0):
+        p = torch.nn.Parameter(torch.zeros(1, dtype=torch.float64))
+        opt = torch.optim.SGD([p], lr=base)
+        sch = torch.optim.lr_scheduler.MultiStepLR(opt, milestones=list(milestones), gamma=gamma)
+        for _ in range(epochs_done):
+            opt.step()
+            sch.step()
+        return opt, sch
+
+    for s in range(len(lrs)):
+        opt, sch = make(lrs[s])
+        for i in range(N):
+            if n_p is not None and i == n_p:
+                assert n_p % spe == 0
+                opt, sch = make(lr_np, n_p // spe)
+            want = opt.param_groups[0]["lr"]
+            assert Pl.learning_rate(hp, s, i, n_p) == pytest.approx(want, rel=1e-12), (s, i)
+            opt.step()
+            if (i + 1) % spe == 0:
+                sch.step()

@@ -12,7 +12,14 @@ import pst_workloads as W
 from oracle import layers as Lx, network as Net, pipeline as Pl
 from tests.parity import flat_params, tensor_errors, loss_errors, hparams, stage_errors
 
-DT = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": None, "tf32": "tf32", "bf16x2": "bf16x2", "tf32x3": "tf32x3"}[sys.argv[1] if len(sys.argv) > 1 else "bf16"]
+MODES = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": None, "tf32": "tf32", "bf16x2": "bf16x2", "tf32x3": "tf32x3"}
+DT = MODES[sys.argv[1] if __name__ == "__main__" and len(sys.argv) > 1 else "tf32x3"]
+
+
+def set_mode(name):
+    """Select the emulated storage/product precision (importers; the CLI takes it as argv[1])."""
+    global DT
+    DT = MODES[name]
 
 def _b(a):
     return torch.from_numpy(np.asarray(a, dtype=np.float64)).to(torch.bfloat16).double().numpy()
@@ -105,19 +112,24 @@ def run(net, ppv, B, N, lr, wd, emu):
     pl = Net.unflatten(net.layers, flat)
     return Pl.run_clocked(st, [pl[a:b] for a, b in bounds], data, hparams(lr, K, lr[-1], 0.9, wd), snapshot=True)
 
-CASES = [("tiny_cnn", W.tiny_cnn(hw=8), (), 32, 8, [0.05], 5e-4),
-                                      ("tiny_resnet", W.tiny_resnet(width=16, hw=8, n=1), (), 32, 8, [0.1], 1e-4),
-                                      ("lenet5", W.lenet5(), (1,), 64, 10, [0.01, 0.01], 5e-4)]
-if len(sys.argv) > 2 and sys.argv[2] == "deep":   # the deep-BN cases judged per stage (AMB-21b)
-    CASES = [("resnet20_k1", W.resnet_cifar(20), (), 32, 8, [0.01], 1e-4),
-             ("resnet110_k2", W.resnet_cifar(110), (47,), 32, 5, [0.01, 0.01], 1e-4)]
-if len(sys.argv) > 2 and sys.argv[2] == "big":
-    CASES = [("lenet5_k2_20", W.lenet5(), (1,), 64, 20, [0.01, 0.01], 5e-4),
-             ("resnet20_k2", W.resnet_cifar(20), (7,), 128, 12, [0.001, 0.1], 1e-4)]
-for name, net, ppv, B, N, lr, wd in CASES:
-    ref = run(net, ppv, B, N, lr, wd, False)
-    emu = run(net, ppv, B, N, lr, wd, True)
-    errs = [tensor_errors(net, flat_params(net, e), flat_params(net, r)) for e, r in zip(emu.snapshots, ref.snapshots)]
-    serrs = [stage_errors(net, ppv, flat_params(net, e), flat_params(net, r))[0] for e, r in zip(emu.snapshots, ref.snapshots)]
-    print(sys.argv[1:], name, "loss err %.2e" % loss_errors(emu.losses, ref.losses), " ".join("%.1e(%s)" % e for e in errs[:N]),
-          "| per stage max %.1e" % max(serrs), flush=True)
+def main():
+    CASES = [("tiny_cnn", W.tiny_cnn(hw=8), (), 32, 8, [0.05], 5e-4),
+                                          ("tiny_resnet", W.tiny_resnet(width=16, hw=8, n=1), (), 32, 8, [0.1], 1e-4),
+                                          ("lenet5", W.lenet5(), (1,), 64, 10, [0.01, 0.01], 5e-4)]
+    if len(sys.argv) > 2 and sys.argv[2] == "deep":   # the deep-BN cases judged per stage (AMB-21b)
+        CASES = [("resnet20_k1", W.resnet_cifar(20), (), 32, 8, [0.01], 1e-4),
+                 ("resnet110_k2", W.resnet_cifar(110), (47,), 32, 5, [0.01, 0.01], 1e-4)]
+    if len(sys.argv) > 2 and sys.argv[2] == "big":
+        CASES = [("lenet5_k2_20", W.lenet5(), (1,), 64, 20, [0.01, 0.01], 5e-4),
+                 ("resnet20_k2", W.resnet_cifar(20), (7,), 128, 12, [0.001, 0.1], 1e-4)]
+    for name, net, ppv, B, N, lr, wd in CASES:
+        ref = run(net, ppv, B, N, lr, wd, False)
+        emu = run(net, ppv, B, N, lr, wd, True)
+        errs = [tensor_errors(net, flat_params(net, e), flat_params(net, r)) for e, r in zip(emu.snapshots, ref.snapshots)]
+        serrs = [stage_errors(net, ppv, flat_params(net, e), flat_params(net, r))[0] for e, r in zip(emu.snapshots, ref.snapshots)]
+        print(sys.argv[1:], name, "loss err %.2e" % loss_errors(emu.losses, ref.losses), " ".join("%.1e(%s)" % e for e in errs[:N]),
+              "| per stage max %.1e" % max(serrs), flush=True)
+
+
+if __name__ == "__main__":
+    main()
