@@ -68,7 +68,7 @@ typedef enum { PST_POOL_NONE = 0, PST_POOL_MAX2 = 1, PST_POOL_GAP = 2 } pst_pool
 /* One weighted layer with the non-weighted ops that follow it, applied in this
  * order: y = conv/fc(x) (+bias); BN_train(y) if bn; + shortcut(block input) if
  * residual (identity, or option A: stride-2 subsample + equal zero channel pad,
- * when shapes differ); ReLU if relu; pool.  block_begin marks a layer whose
+ * when shapes differ); ReLU if relu; dropout if dropout > 0; pool.  block_begin marks a layer whose
  * INPUT is the residual block input of the next residual layer. */
 typedef struct {
   int32_t kind;        /* pst_layer_kind */
@@ -80,6 +80,12 @@ typedef struct {
   int32_t residual;    /* 0/1 */
   int32_t relu;        /* 0/1 */
   int32_t pool;        /* pst_pool */
+  float dropout;       /* drop probability p in [0, 1) applied after the ReLU, before the pool
+                          (VGG-16 "batch normalization and dropout"; needs relu).  Inverted
+                          dropout with the counter-based masks of DESIGN.md (reading AMB-16b):
+                          key = fmix32(seed ^ fmix32(mb*0x9E3779B9 + (layer+1)*0x632BE5AB)), element
+                          e (logical NCHW index) kept iff fmix32(e ^ key) >= floor(p * 2^32), kept
+                          values scaled by 1/(1-p); mb = the mini-batch index, layer = 0-based. */
 } pst_layer;
 
 typedef struct {
@@ -122,6 +128,7 @@ typedef struct {
                                 lr(i) = base (1 + inv_gamma i)^(-inv_power), i = the gradient's
                                 mini-batch index (reading AMB-8)                          */
   float inv_gamma, inv_power;
+  uint32_t dropout_seed;     /* seed of the dropout masks (pst_layer.dropout) */
 } pst_hparams;
 
 /* Distributed mode: one process per stage (rank == stage), NCCL send/recv

@@ -133,6 +133,43 @@ def relu_backward(g, mask):
     return g * mask
 
 
+# --------------------------------------------------------------------------- dropout
+def _fmix32(h):
+    """MurmurHash3's 32-bit finaliser on uint32 arrays (wrap-around arithmetic)."""
+    h = np.asarray(h, dtype=np.uint32).copy()
+    h ^= h >> np.uint32(16)
+    h *= np.uint32(0x85EBCA6B)
+    h ^= h >> np.uint32(13)
+    h *= np.uint32(0xC2B2AE35)
+    h ^= h >> np.uint32(16)
+    return h
+
+
+def dropout_threshold(p):
+    """Integer keep threshold of drop probability p (p read as float32, as the ABI passes it):
+    an element is dropped iff its 32-bit hash is < floor(p * 2^32)."""
+    return min(2 ** 32 - 1, int(np.floor(float(np.float32(p)) * 2.0 ** 32)))
+
+
+def dropout_mask(seed, mb, layer, shape, p):
+    """Inverted dropout (VGG-16 "batch normalization and dropout ... throughout", PAPER.md L288,
+    SURVEY f-3) with a counter-based generator shared by definition with the CUDA path: for
+    mini-batch `mb`, 0-based weighted layer `layer` and the element's logical NCHW index e,
+        key = fmix32(seed ^ fmix32(mb * 0x9E3779B9 + (layer + 1) * 0x632BE5AB))
+        u   = fmix32(e ^ key);   keep iff u >= floor(p * 2^32)
+    (uint32 wrap-around arithmetic).  The mask depends only on (seed, mb, layer, e): the stale
+    forward of mini-batch i draws exactly the mask a non-pipelined forward of i would.
+    Returns 0 or 1/(1-p) per element (float64)."""
+    with np.errstate(over="ignore"):
+        pre = np.uint32((int(mb) * 0x9E3779B9 + (int(layer) + 1) * 0x632BE5AB) & 0xFFFFFFFF)
+        key = _fmix32(np.uint32(int(seed) & 0xFFFFFFFF) ^ _fmix32(pre))
+        e = (np.arange(int(np.prod(shape)), dtype=np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+        u = _fmix32(e ^ key)
+    keep = u >= np.uint32(dropout_threshold(p)) if dropout_threshold(p) > 0 else np.ones(u.shape, bool)
+    scale = 1.0 / (1.0 - float(np.float32(p)))
+    return (keep.astype(np.float64) * scale).reshape(shape)
+
+
 # --------------------------------------------------------------------------- pooling
 def maxpool2_forward(x):
     """2x2 max-pool, stride 2.  Tie-break: first maximum in row-major window

@@ -58,31 +58,32 @@ def n_params(layer_specs):
 
 # --------------------------------------------------------------------------- partition
 def partition(layer_specs, ppv):
-    """PPV -> list of (start, end) 0-based layer ranges, validated.
-
-    Valid: strictly increasing, each p in [1, L-1], and no boundary inside a
-    residual block (a block opened by `block_begin` must close with its
-    `residual` layer in the same stage; mid-block registers are reading
-    AMB-14, unsupported)."""
+    """PPV -> list of (start, end) 0-based layer ranges, validated: strictly increasing, each p in
+    [1, L-1].  A boundary may fall inside a residual block (the paper's ResNet-20 PPV (5,12,17),
+    P:L179 section 6.4, and its fine-grained placements "within residual function blocks", P:L135
+    section 6.3): the register pair then carries two tensors -- see CNNStage (reading AMB-14)."""
     Lcount = len(layer_specs)
     ppv = [int(p) for p in ppv]
     if any(p < 1 or p > Lcount - 1 for p in ppv):
         raise ValueError(f"PPV entries must be in [1, {Lcount - 1}]: {ppv}")
     if any(b <= a for a, b in zip(ppv, ppv[1:])):
         raise ValueError(f"PPV must be strictly increasing: {ppv}")
-    open_at = []
-    is_open = False
+    bounds = [0] + ppv + [Lcount]
+    return [(bounds[s], bounds[s + 1]) for s in range(len(bounds) - 1)]
+
+
+def open_block_at(layer_specs):
+    """open[p]: True if a residual block is open between layers p-1 and p (0-based), i.e. a
+    register pair after 1-based layer p sits inside a residual block (mid-block register)."""
+    out, is_open = [], False
     for L in layer_specs:
-        open_at.append(is_open)          # open state *before* this layer
+        out.append(is_open)
         if L.block_begin:
             is_open = True
         if L.residual:
             is_open = False
-    for p in ppv:
-        if open_at[p]:
-            raise ValueError(f"PPV boundary after layer {p} splits a residual block")
-    bounds = [0] + ppv + [Lcount]
-    return [(bounds[s], bounds[s + 1]) for s in range(len(bounds) - 1)]
+    out.append(False)
+    return out
 
 
 def stale_weight_percentage(layer_specs, ppv):
@@ -102,9 +103,15 @@ class CNNStage:
     (the *current* weights, PAPER.md L63/L75 + reading AMB-2).
     """
 
-    def __init__(self, layer_specs, first_stage=False, bn_momentum=0.1, bn_eps=1e-5):
+    def __init__(self, layer_specs, first_stage=False, bn_momentum=0.1, bn_eps=1e-5, dropout_seed=0, layer0=0):
+        """Mid-block registers (reading AMB-14): a stage whose first layer lies inside a residual
+        block receives (activation, block input) and, in the backward, returns (gradient of the
+        activation, gradient of the block input through the shortcut); a stage that ends inside a
+        block emits (activation, block input) and receives the same pair of gradients."""
         self.layers = list(layer_specs)
         self.first_stage = first_stage
+        self.dropout_seed = dropout_seed   # counter-based dropout masks (layers.dropout_mask)
+        self.layer0 = layer0               # network index of this stage's first layer
         self.bn_momentum = bn_momentum
         self.bn_eps = bn_eps
         self.state = [
@@ -112,10 +119,14 @@ class CNNStage:
             for L in self.layers
         ]
 
-    def forward(self, params, x):
+    def forward(self, params, x, mb=0):
+        """mb: the mini-batch index (it selects the dropout masks; nothing else depends on it)."""
+        block_in = None
+        if isinstance(x, tuple):                 # mid-block register: (activation, block input)
+            x, block_in = x
+            block_in = np.asarray(block_in, dtype=np.float64)
         a = np.asarray(x, dtype=np.float64)
         caches = []
-        block_in = None
         for L, P, S in zip(self.layers, params, self.state):
             c = {"x": a}
             if L.block_begin:
@@ -135,26 +146,38 @@ class CNNStage:
                 y = y + Lx.shortcut_forward(block_in, y.shape)
             if L.relu:
                 y, c["mask"] = Lx.relu_forward(y)
+            if getattr(L, "dropout", 0.0) > 0.0:
+                c["drop"] = Lx.dropout_mask(self.dropout_seed, mb, self.layer0 + len(caches), y.shape, L.dropout)
+                y = y * c["drop"]
             if L.pool == "max2":
                 c["pool_in_shape"] = y.shape
                 y, c["arg"] = Lx.maxpool2_forward(y)
             elif L.pool == "gap":
                 c["pool_in_shape"] = y.shape
                 y = Lx.gap_forward(y)
+            if L.residual:
+                block_in = None                  # the block is closed
             caches.append(c)
             a = y
+        if block_in is not None:                 # the stage ends inside a block
+            return (a, block_in), caches
         return a, caches
 
     def backward(self, params, caches, g_out):
+        g_shortcut = None
+        if isinstance(g_out, tuple):             # the stage ends inside a block
+            g_out, g_shortcut = g_out
+            g_shortcut = np.asarray(g_shortcut, dtype=np.float64)
         g = np.asarray(g_out, dtype=np.float64)
         grads = [None] * len(self.layers)
-        g_shortcut = None
         for idx in range(len(self.layers) - 1, -1, -1):
             L, P, c = self.layers[idx], params[idx], caches[idx]
             if L.pool == "max2":
                 g = Lx.maxpool2_backward(g, c["arg"], c["pool_in_shape"])
             elif L.pool == "gap":
                 g = Lx.gap_backward(g, c["pool_in_shape"])
+            if "drop" in c:
+                g = g * c["drop"]
             if L.relu:
                 g = Lx.relu_backward(g, c["mask"])
             if L.residual:
@@ -175,6 +198,8 @@ class CNNStage:
                 g_shortcut = None
             grads[idx] = gr
             g = gx
+        if g_shortcut is not None:               # the stage starts inside a block
+            return (g, g_shortcut), grads
         return g, grads
 
     def bn_stats(self):

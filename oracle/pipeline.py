@@ -128,7 +128,7 @@ def run_versioned(stages, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce, 
         for s in range(K):
             ver = forward_version(K, s, i, n_p)
             log.append((None, s, "F", i, ver))
-            a, c = stages[s].forward(hist[s][ver], a)
+            a, c = stages[s].forward(hist[s][ver], a, mb=i)
             caches.append(c)
         loss, g = loss_fn(a, y)
         losses.append(loss)
@@ -192,7 +192,7 @@ def run_clocked(stages, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce, n_
             if 0 <= f < n_pipe:
                 a_in = batches[f][0] if s == 0 else inbox_f[s].pop(f)
                 log.append((t, s, "F", f, v[s]))
-                out, cache = stages[s].forward(W[s], a_in)
+                out, cache = stages[s].forward(W[s], a_in, mb=f)
                 ring[s][f] = cache
                 assert len(ring[s]) <= ring_depth(K, s), (t, s, len(ring[s]))
                 if s == K - 1:
@@ -213,7 +213,7 @@ def run_clocked(stages, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce, n_
         caches = []
         for s in range(K):
             log.append((t, s, "F", i, v[s]))
-            a, c = stages[s].forward(W[s], a)
+            a, c = stages[s].forward(W[s], a, mb=i)
             caches.append(c)
         losses[i], g = loss_fn(a, batches[i][1])
         for s in range(K - 1, -1, -1):
@@ -234,7 +234,7 @@ def run_sgd(stage, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce):
     mom = _zeros_like(params0)
     losses = []
     for i, (x, y) in enumerate(batches):
-        out, cache = stage.forward(W, x)
+        out, cache = stage.forward(W, x, mb=i)
         loss, g = loss_fn(out, y)
         losses.append(loss)
         _, G = stage.backward(W, cache, g)

@@ -29,7 +29,7 @@ class PstError(RuntimeError):
 
 class _Layer(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("kind", "cin", "cout", "k", "stride", "pad", "bias", "bn",
-                                         "block_begin", "residual", "relu", "pool")]
+                                         "block_begin", "residual", "relu", "pool")] + [("dropout", C.c_float)]
 
 
 class _Net(C.Structure):
@@ -48,7 +48,7 @@ class _HParams(C.Structure):
                 ("n_milestones", C.c_int32), ("milestone_epochs", C.POINTER(C.c_int64)),
                 ("gamma", C.c_float), ("steps_per_epoch", C.c_int64),
                 ("solver", C.c_int32), ("nesterov", C.c_int32), ("lr_policy", C.c_int32),
-                ("inv_gamma", C.c_float), ("inv_power", C.c_float)]
+                ("inv_gamma", C.c_float), ("inv_power", C.c_float), ("dropout_seed", C.c_uint32)]
 
 
 class _Dist(C.Structure):
@@ -130,7 +130,8 @@ def net_struct(net, params: Optional[np.ndarray] = None):
     arr = (_Layer * len(net.layers))()
     for i, L in enumerate(net.layers):
         arr[i] = _Layer(kinds[L.kind], L.cin, L.cout, L.k, L.stride, L.pad, int(L.bias), int(L.bn),
-                        int(L.block_begin), int(L.residual), int(L.relu), pools[L.pool])
+                        int(L.block_begin), int(L.residual), int(L.relu), pools[L.pool],
+                        float(getattr(L, "dropout", 0.0)))
     keep = [arr]
     n = _Net()
     n.n_layers = len(net.layers)
@@ -194,7 +195,8 @@ class Pipeline:
                  milestones: Sequence[int] = (), gamma: float = 0.1, steps_per_epoch: int = 1 << 62,
                  devices: Optional[Sequence[int]] = None, rank: Optional[int] = None,
                  nccl_id: Optional[bytes] = None, solver: str = "torch", nesterov: bool = False,
-                 lr_policy: str = "multistep", inv_gamma: float = 0.0, inv_power: float = 0.0):
+                 lr_policy: str = "multistep", inv_gamma: float = 0.0, inv_power: float = 0.0,
+                 dropout_seed: int = 0):
         L = lib()
         self.net = net
         self.K = len(ppv) + 1
@@ -206,7 +208,7 @@ class Pipeline:
         hp = _HParams(batch, momentum, weight_decay, C.cast(lrs, C.POINTER(C.c_float)), lr_nonpipelined,
                       len(milestones), C.cast(ms, C.POINTER(C.c_int64)), gamma, steps_per_epoch,
                       {"torch": 0, "caffe": 1}[solver], int(bool(nesterov)),
-                      {"multistep": 0, "inv": 1}[lr_policy], inv_gamma, inv_power)
+                      {"multistep": 0, "inv": 1}[lr_policy], inv_gamma, inv_power, dropout_seed & 0xFFFFFFFF)
         self._keep_hp = (lrs, ms)
         dist = None
         if rank is not None:

@@ -63,6 +63,7 @@ struct TsArgs {
   int knob;                  // experiment switches (PST_TS_KNOB), 0 in production
   const act_t* bz; const act_t* by; const float* bsaved; double* bsums;   // fused bwd_pre (EPI_DGRAD)
   int bfuse, brelu, bbn;
+  float bscale;
 };
 
 __device__ __forceinline__ unsigned long long ts_gtime() {
@@ -425,10 +426,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             } else if (a.brelu) {
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj) {
-                u[4 * jj] = zv[jj].x > 0.f ? u[4 * jj] : 0.f;
-                u[4 * jj + 1] = zv[jj].y > 0.f ? u[4 * jj + 1] : 0.f;
-                u[4 * jj + 2] = zv[jj].z > 0.f ? u[4 * jj + 2] : 0.f;
-                u[4 * jj + 3] = zv[jj].w > 0.f ? u[4 * jj + 3] : 0.f;
+                u[4 * jj] = zv[jj].x > 0.f ? u[4 * jj] * a.bscale : 0.f;
+                u[4 * jj + 1] = zv[jj].y > 0.f ? u[4 * jj + 1] * a.bscale : 0.f;
+                u[4 * jj + 2] = zv[jj].z > 0.f ? u[4 * jj + 2] * a.bscale : 0.f;
+                u[4 * jj + 3] = zv[jj].w > 0.f ? u[4 * jj + 3] * a.bscale : 0.f;
               }
             }
           }
@@ -577,6 +578,7 @@ bool conv_ts(const ConvSpec& c, cudaStream_t st) {
   a.dbg = c.dbg;
   a.bz = c.bz; a.by = c.by; a.bsaved = c.bsaved; a.bsums = c.bsums;
   a.bfuse = c.bfuse; a.brelu = c.brelu; a.bbn = c.bbn;
+  a.bscale = c.bscale == 0.f ? 1.f : c.bscale;
   { static const char* kn = std::getenv("PST_TS_KNOB"); a.knob = kn ? std::atoi(kn) : 0; }
   // band box: (Wb*EPC, Hb, nb images, KC/EPC planes) of the planar input, zero outside
   uint64_t dims[4] = {(uint64_t)c.W * kEPC, (uint64_t)c.H, (uint64_t)c.N, (uint64_t)c.Cinp / kEPC};

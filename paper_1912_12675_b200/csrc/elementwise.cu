@@ -299,7 +299,7 @@ __global__ void bwd_pre_kernel(const BwdPreSpec s) {
         const int p = base + u * kBlock + threadIdx.x;
         if (p >= npix) continue;
 #pragma unroll
-        for (int j = 0; j < E; ++j) g[u][j] = z[u][j] > 0.f ? g[u][j] : 0.f;
+        for (int j = 0; j < E; ++j) g[u][j] = z[u][j] > 0.f ? g[u][j] * s.rscale : 0.f;   // dropout scale (or 1)
       }
     }
     float y[kU][E];
@@ -636,6 +636,48 @@ __global__ void wgrad_reduce_kernel(const float* part, int ksplit, int Coutp, in
 
 // ------------------------------------------------------------------ launchers
 // pixel-chunk grid for the plane-blocked kernels: about 4 resident blocks per SM in total
+// ------------------------------------------------------------------ dropout (SURVEY f-3)
+// Counter-based inverted dropout, the definition DESIGN.md gives (reading AMB-16b):
+//   key = fmix32(seed ^ fmix32(mb * 0x9E3779B9 + (layer + 1) * 0x632BE5AB))
+//   keep element e (logical NCHW index) iff fmix32(e ^ key) >= thresh; kept values *= scale.
+// Applied in place to the post-ReLU tensor z; mb is the stage's forward counter (device memory, so
+// the captured step graphs stay valid).  The backward needs no generator: z > 0 <=> kept and
+// ReLU-active, and bwd_pre / the fused dgrad epilogue multiply the gradient by `scale` there.
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
+  return h;
+}
+
+__global__ void dropout_fwd_kernel(act_t* __restrict__ z, int N, int HW, int Cp, int C, uint32_t seed, int layer,
+                                   uint32_t thresh, float scale, const int64_t* __restrict__ fmb) {
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t mb = (uint32_t)(*fmb);
+  const uint32_t key = fmix32(seed ^ fmix32(mb * 0x9E3779B9u + (uint32_t)(layer + 1) * 0x632BE5ABu));
+  const int64_t npix = (int64_t)N * HW;
+  const int64_t nvec = npix * (Cp / E);
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const int plane = (int)(v / npix);
+    const int64_t p = v - (int64_t)plane * npix;
+    const int n = (int)(p / HW), hw = (int)(p - (int64_t)n * HW);
+    float f[E];
+    ldv(z + v * E, f);
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int c = plane * E + i;
+      const uint32_t e = (uint32_t)(((int64_t)n * C + c) * HW + hw);
+      f[i] = (c < C && fmix32(e ^ key) >= thresh) ? f[i] * scale : 0.f;
+    }
+    stv(z + v * E, f);
+  }
+}
+
+__global__ void counter_inc_kernel(int64_t* c) {
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0 && blockIdx.x == 0) *c += 1;
+}
+
 static dim3 plane_grid(int npix, int planes) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -680,6 +722,21 @@ void gap_fwd(const act_t* in, act_t* out, int N, int H, int W, int Cp, cudaStrea
   PST_CUDA(launch_k(gap_kernel, dim3(grid_for(nvec)), dim3(kBlock), 0, st, in, out, N, H, W, Cp));
   PST_CUDA(cudaGetLastError());
   prof::end(st, prof::POOL, (double)nvec * 16 * (H * W + 1), 0);
+}
+
+void dropout_fwd(act_t* z, int N, int H, int W, int Cp, int C, uint32_t seed, int layer, uint32_t thresh, float scale,
+                 const int64_t* fmb, cudaStream_t st) {
+  const int64_t nvec = (int64_t)N * H * W * (Cp / E);
+  prof::begin(st);
+  PST_CUDA(launch_k(dropout_fwd_kernel, dim3(grid_for(nvec)), dim3(kBlock), 0, st, z, N, H * W, Cp, C, seed, layer,
+                    thresh, scale, fmb));
+  prof::end(st, prof::MISC, 2.0 * nvec * 16, 0.0);
+}
+
+void counter_inc(int64_t* c, cudaStream_t st) {
+  prof::begin(st);
+  PST_CUDA(launch_k(counter_inc_kernel, dim3(1), dim3(32), 0, st, c));
+  prof::end(st, prof::MISC, 16.0, 0.0);
 }
 
 void bwd_pre(const BwdPreSpec& s, cudaStream_t st) {

@@ -40,6 +40,7 @@ struct ConvSpec {
   // and sums[c] += (sum gpre, sum gpre * (by - mean) * invstd) with bsaved = (mean, invstd)
   const act_t* bz; const act_t* by; const float* bsaved; double* bsums;
   int bfuse, brelu, bbn;
+  float bscale;             // fused bwd_pre: dropout scale of the lower layer where z > 0 (0 = 1)
   unsigned long long* dbg;  // optional device timeline buffer [8][256] (CTA 0), debug only
 };
 void conv_tc(const ConvSpec& c, cudaStream_t st);
@@ -103,12 +104,19 @@ void gap_fwd(const act_t* in, act_t* out, int N, int H, int W, int Cp, cudaStrea
 struct BwdPreSpec {
   const act_t* gout; int pool; const uint8_t* arg;  // pool: 0 none, 1 max2, 2 gap
   const act_t* z; int relu;
+  float rscale;             // where z > 0: the layer's dropout scale 1/(1-p), else 1
   const act_t* y; const float* saved; int bn;
   act_t* gpre; int N, H, W, Cp, C;
   double* sums;             // [Cp][2]
   int gout_f32;             // gout is float (loss gradient) instead of act_t
 };
 void bwd_pre(const BwdPreSpec& s, cudaStream_t st);
+
+// Counter-based inverted dropout in place on z (reading AMB-16b); fmb: device counter
+// holding the mini-batch index of the running forward.
+void dropout_fwd(act_t* z, int N, int H, int W, int Cp, int C, uint32_t seed, int layer, uint32_t thresh, float scale,
+                 const int64_t* fmb, cudaStream_t st);
+void counter_inc(int64_t* c, cudaStream_t st);
 
 // BN backward apply: gy = gamma_cur*invstd/M * (M*gpre - S1 - xhat*S2)
 struct BnBwdSpec {

@@ -51,6 +51,8 @@ NetInfo derive_net(const pst_net& net) {
     }
     li.Coutp = rup16(L.cout);
     if (L.bias && L.bn) throw Unsupported(at + "bias followed by BatchNorm");
+    PST_CHECK_ARG(L.dropout >= 0.f && L.dropout < 1.f, at + "dropout must be in [0, 1)");
+    if (L.dropout > 0.f) PST_CHECK_ARG(L.relu, at + "dropout needs a ReLU before it (build restriction)");
     if (L.residual) {
       PST_CHECK_ARG(open_block >= 0, at + "residual without an open block");
       PST_CHECK_ARG(L.bn, at + "residual layers must have BN (build restriction)");
@@ -122,15 +124,19 @@ std::vector<std::pair<int, int>> partition(const NetInfo& net, int K, const int3
     b.push_back(p);
   }
   b.push_back(L);
-  // a boundary before layer p must not split a residual block (AMB-14)
-  for (size_t i = 1; i + 1 < b.size(); ++i) {
-    const int p = b[i];
-    for (int j = 0; j < p; ++j) {
-      const LayerInfo& li = net.layers[j];
-      if (li.spec.block_begin && li.block_end >= p)
-        throw Unsupported("PPV boundary after layer " + std::to_string(p) +
-                          " splits a residual block (mid-block registers not supported)");
-    }
+  // A boundary may fall inside a residual block (mid-block register pair, reading
+  // AMB-14): the register then carries the block input beside the activation (forward) and the
+  // shortcut gradient beside the input gradient (backward).  Build restriction: at most one
+  // boundary inside any block (every block of the supported nets has two weighted layers).
+  for (int j = 0; j < L; ++j) {
+    const LayerInfo& li = net.layers[j];
+    if (!li.spec.block_begin || li.block_end < 0) continue;
+    int inside = 0;
+    for (size_t i = 1; i + 1 < b.size(); ++i)
+      if (b[i] > j && b[i] <= li.block_end) ++inside;
+    if (inside > 1)
+      throw Unsupported("more than one PPV boundary inside the residual block of layers " + std::to_string(j + 1) +
+                        ".." + std::to_string(li.block_end + 1));
   }
   std::vector<std::pair<int, int>> r;
   for (int s = 0; s < K; ++s) r.push_back({b[s], b[s + 1]});

@@ -135,16 +135,20 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
     S->enqueue_backward((int)(p.bwd_mb % S->R), (int)(p.bwd_mb & 1), st);
     if (s > 0 && !c->dist) {
       Stage* D = c->stage(s - 1);
-      PST_CUDA(cudaMemcpyAsync(D->dbuf((int)(p.bwd_mb & 1)), S->dgrad_out(), D->output_bytes(),
-                               cudaMemcpyDefault, st));
+      const int par = (int)(p.bwd_mb & 1);
+      PST_CUDA(cudaMemcpyAsync(D->dbuf(par), S->dgrad_out(), D->output_bytes(), cudaMemcpyDefault, st));
+      if (S->starts_mid())   // mid-block register: the shortcut gradient goes back too
+        PST_CUDA(cudaMemcpyAsync(D->dbuf2(par), S->sgrad_out(), S->sgrad_bytes(), cudaMemcpyDefault, st));
     }
   }
   if (p.fwd_mb >= 0) {
     S->enqueue_forward((int)(p.fwd_mb % S->R), st);
     if (s < K - 1 && !c->dist) {
       Stage* D = c->stage(s + 1);
-      PST_CUDA(cudaMemcpyAsync(D->input_slot((int)(p.fwd_mb % D->R)), S->output_slot((int)(p.fwd_mb % S->R)),
-                               S->output_bytes(), cudaMemcpyDefault, st));
+      const int ss = (int)(p.fwd_mb % S->R), ds = (int)(p.fwd_mb % D->R);
+      PST_CUDA(cudaMemcpyAsync(D->input_slot(ds), S->output_slot(ss), S->output_bytes(), cudaMemcpyDefault, st));
+      if (S->ends_mid())     // mid-block register: the block input goes forward too
+        PST_CUDA(cudaMemcpyAsync(D->input2_slot(ds), S->block_out(ss), S->block_out_bytes(), cudaMemcpyDefault, st));
     }
   }
   if (c->dist) {
@@ -154,14 +158,26 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
     const bool recv_b = s < K - 1 && next_stage.bwd_mb >= 0;
     if (send_f || recv_f || send_b || recv_b) {
       PST_NCCL(ncclGroupStart());
-      if (send_f)
-        PST_NCCL(ncclSend(S->output_slot((int)(p.fwd_mb % S->R)), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
-      if (recv_f)
-        PST_NCCL(ncclRecv(S->input_slot((int)(prev_stage.fwd_mb % S->R)), S->input_bytes(), ncclUint8, s - 1,
-                          c->comm, st));
-      if (send_b) PST_NCCL(ncclSend(S->dgrad_out(), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
-      if (recv_b)
-        PST_NCCL(ncclRecv(S->dbuf((int)(next_stage.bwd_mb & 1)), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+      if (send_f) {
+        const int ss = (int)(p.fwd_mb % S->R);
+        PST_NCCL(ncclSend(S->output_slot(ss), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+        if (S->ends_mid()) PST_NCCL(ncclSend(S->block_out(ss), S->block_out_bytes(), ncclUint8, s + 1, c->comm, st));
+      }
+      if (recv_f) {
+        const int ds = (int)(prev_stage.fwd_mb % S->R);
+        PST_NCCL(ncclRecv(S->input_slot(ds), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
+        if (S->starts_mid())
+          PST_NCCL(ncclRecv(S->input2_slot(ds), S->block_out_bytes(), ncclUint8, s - 1, c->comm, st));
+      }
+      if (send_b) {
+        PST_NCCL(ncclSend(S->dgrad_out(), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
+        if (S->starts_mid()) PST_NCCL(ncclSend(S->sgrad_out(), S->sgrad_bytes(), ncclUint8, s - 1, c->comm, st));
+      }
+      if (recv_b) {
+        const int par = (int)(next_stage.bwd_mb & 1);
+        PST_NCCL(ncclRecv(S->dbuf(par), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+        if (S->ends_mid()) PST_NCCL(ncclRecv(S->dbuf2(par), S->sgrad_bytes(), ncclUint8, s + 1, c->comm, st));
+      }
       PST_NCCL(ncclGroupEnd());
     }
   }
@@ -172,28 +188,48 @@ static void enqueue_np(pst_ctx* c, int s, int64_t i, bool fwd, cudaStream_t st) 
   Stage* S = c->stage(s);
   const int K = c->K;
   const int slot = (int)(i % S->R);
+  const int par = (int)(i & 1);
   if (fwd) {
-    if (c->dist && s > 0) PST_NCCL(ncclRecv(S->input_slot(slot), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
+    if (c->dist && s > 0) {
+      PST_NCCL(ncclGroupStart());
+      PST_NCCL(ncclRecv(S->input_slot(slot), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
+      if (S->starts_mid()) PST_NCCL(ncclRecv(S->input2_slot(slot), S->block_out_bytes(), ncclUint8, s - 1, c->comm, st));
+      PST_NCCL(ncclGroupEnd());
+    }
     S->enqueue_forward(slot, st);
     if (s < K - 1) {
       if (c->dist) {
+        PST_NCCL(ncclGroupStart());
         PST_NCCL(ncclSend(S->output_slot(slot), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+        if (S->ends_mid()) PST_NCCL(ncclSend(S->block_out(slot), S->block_out_bytes(), ncclUint8, s + 1, c->comm, st));
+        PST_NCCL(ncclGroupEnd());
       } else {
         Stage* D = c->stage(s + 1);
-        PST_CUDA(cudaMemcpyAsync(D->input_slot((int)(i % D->R)), S->output_slot(slot), S->output_bytes(),
-                                 cudaMemcpyDefault, st));
+        const int ds = (int)(i % D->R);
+        PST_CUDA(cudaMemcpyAsync(D->input_slot(ds), S->output_slot(slot), S->output_bytes(), cudaMemcpyDefault, st));
+        if (S->ends_mid())
+          PST_CUDA(cudaMemcpyAsync(D->input2_slot(ds), S->block_out(slot), S->block_out_bytes(), cudaMemcpyDefault, st));
       }
     }
   } else {
-    if (c->dist && s < K - 1)
-      PST_NCCL(ncclRecv(S->dbuf((int)(i & 1)), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
-    S->enqueue_backward(slot, (int)(i & 1), st);
+    if (c->dist && s < K - 1) {
+      PST_NCCL(ncclGroupStart());
+      PST_NCCL(ncclRecv(S->dbuf(par), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+      if (S->ends_mid()) PST_NCCL(ncclRecv(S->dbuf2(par), S->sgrad_bytes(), ncclUint8, s + 1, c->comm, st));
+      PST_NCCL(ncclGroupEnd());
+    }
+    S->enqueue_backward(slot, par, st);
     if (s > 0) {
       if (c->dist) {
+        PST_NCCL(ncclGroupStart());
         PST_NCCL(ncclSend(S->dgrad_out(), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
+        if (S->starts_mid()) PST_NCCL(ncclSend(S->sgrad_out(), S->sgrad_bytes(), ncclUint8, s - 1, c->comm, st));
+        PST_NCCL(ncclGroupEnd());
       } else {
         Stage* D = c->stage(s - 1);
-        PST_CUDA(cudaMemcpyAsync(D->dbuf((int)(i & 1)), S->dgrad_out(), D->output_bytes(), cudaMemcpyDefault, st));
+        PST_CUDA(cudaMemcpyAsync(D->dbuf(par), S->dgrad_out(), D->output_bytes(), cudaMemcpyDefault, st));
+        if (S->starts_mid())
+          PST_CUDA(cudaMemcpyAsync(D->dbuf2(par), S->sgrad_out(), S->sgrad_bytes(), cudaMemcpyDefault, st));
       }
     }
   }

@@ -2,6 +2,7 @@
 #include "stage.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -20,6 +21,13 @@ static bool skip(const char* cls) {
   static const char* env = std::getenv("PST_SKIP");
   return env != nullptr && std::strstr(env, cls) != nullptr;
 }
+
+// Dropout threshold and scale from the float32 probability (pst.h pst_layer.dropout).
+static uint32_t drop_thresh(float p) {
+  const double t = std::floor((double)p * 4294967296.0);
+  return t >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)t;
+}
+static float drop_scale(float p) { return (float)(1.0 / (1.0 - (double)p)); }
 
 template <typename T>
 T* Stage::alloc(size_t n, bool zero) {
@@ -48,11 +56,24 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
   w_ = alloc<float>(n_params);
   v_ = alloc<float>(n_params);
   PST_CUDA(cudaMemcpy(w_, init_params + p_base, n_params * sizeof(float), cudaMemcpyHostToDevice));
+  dseed_ = hp.dropout_seed;
+  for (int l = l0; l < l1; ++l) has_drop_ = has_drop_ || net.layers[l].spec.dropout > 0.f;
+  if (has_drop_) d_fmb_ = alloc<int64_t>(1);   // mini-batch index of the running forward (dropout masks)
 
+  // mid-block registers: the block open across each end of the stage
+  for (int l = 0; l < l0; ++l)
+    if (net.layers[l].spec.block_begin && net.layers[l].block_end >= l0) start_res_ = net.layers[l].block_end;
+  for (int l = l0; l < l1; ++l)
+    if (net.layers[l].spec.block_begin && net.layers[l].block_end >= l1) end_block_ = l;
   // input ring of the stage
   const LayerInfo& f0 = net.layers[l0];
   for (int r = 0; r < R; ++r) xin_.push_back(alloc<act_t>((size_t)B * f0.in_H * f0.in_W * f0.in_Cp));
   bytes_slot += (size_t)B * f0.in_H * f0.in_W * f0.in_Cp * sizeof(act_t);
+  if (starts_mid()) {
+    const LayerInfo& src = net.layers[net.layers[start_res_].block_src];
+    for (int r = 0; r < R; ++r) xin2_.push_back(alloc<act_t>((size_t)B * src.in_H * src.in_W * src.in_Cp));
+    bytes_slot += (size_t)B * src.in_H * src.in_W * src.in_Cp * sizeof(act_t);
+  }
   if (is_first()) xstage_ = alloc<float>((size_t)B * net.in_C * net.in_H * net.in_W);
 
   // per-layer buffers
@@ -118,6 +139,10 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     const size_t ob = (size_t)B * lastl.out_H * lastl.out_W * ((lastl.out_C + 15) / 16 * 16);
     dbuf_[0] = alloc<act_t>(ob);
     dbuf_[1] = alloc<act_t>(ob);
+    if (ends_mid()) {
+      dbuf2_[0] = alloc<act_t>(sgrad_bytes() / sizeof(act_t));
+      dbuf2_[1] = alloc<act_t>(sgrad_bytes() / sizeof(act_t));
+    }
   } else {
     label_ring_n_ = 2 * K + 2;
     label_ring_ = alloc<int32_t>((size_t)label_ring_n_ * B);
@@ -246,6 +271,14 @@ size_t Stage::output_bytes() const {
   const LayerInfo& li = net_.layers[l1 - 1];
   return (size_t)batch_ * li.out_H * li.out_W * ((li.out_C + 15) / 16 * 16) * sizeof(act_t);
 }
+size_t Stage::block_out_bytes() const {   // the block input of the block open at the stage's end
+  const LayerInfo& src = net_.layers[end_block_ >= 0 ? end_block_ : net_.layers[start_res_].block_src];
+  return (size_t)batch_ * src.in_H * src.in_W * src.in_Cp * sizeof(act_t);
+}
+size_t Stage::sgrad_bytes() const {        // the closing residual layer's pre-activation gradient
+  const LayerInfo& e = net_.layers[start_res_ >= 0 ? start_res_ : net_.layers[end_block_].block_end];
+  return (size_t)batch_ * e.Ho * e.Wo * e.Coutp * sizeof(act_t);
+}
 size_t Stage::stage_x_bytes() const {
   return (size_t)batch_ * net_.in_C * net_.in_H * net_.in_W * sizeof(float);
 }
@@ -302,7 +335,7 @@ void Stage::enqueue_forward(int slot, cudaStream_t st) {
       a.relu = li.spec.relu;
       if (li.spec.residual) {
         const LayerInfo& src = net_.layers[li.block_src];
-        a.res = in_tensor(li.block_src, slot);
+        a.res = li.block_src < l0 ? xin2_[slot] : in_tensor(li.block_src, slot);   // mid-block: received
         a.res_mode = li.res_mode;
         a.res_H = src.in_H; a.res_W = src.in_W; a.res_C = src.in_Cp; a.res_Creal = src.in_C;
         a.res_pad = li.res_pad;
@@ -310,6 +343,9 @@ void Stage::enqueue_forward(int slot, cudaStream_t st) {
       if (!skip("bnapply")) bn_apply(a, st);
       ++bn_local;
     }
+    if (li.spec.dropout > 0.f)   // after the ReLU, before the pool (pst.h pst_layer.dropout)
+      dropout_fwd(b.z[slot], B, li.Ho, li.Wo, li.Coutp, li.spec.cout, dseed_, l, drop_thresh(li.spec.dropout),
+                  drop_scale(li.spec.dropout), d_fmb_, st);
     if (li.spec.pool == PST_POOL_MAX2)
       maxpool2_fwd(b.z[slot], b.p[slot], b.arg[slot], B, li.Ho, li.Wo, li.Coutp, st);
     else if (li.spec.pool == PST_POOL_GAP)
@@ -318,6 +354,7 @@ void Stage::enqueue_forward(int slot, cudaStream_t st) {
       softmax_ce(b.zf[slot], label_ring_, label_ring_n_, loss_ring_, fwd_counter_, dz_, B,
                  li.spec.cout, li.Coutp, st);
   }
+  if (has_drop_) counter_inc(d_fmb_, st);
 }
 
 // ------------------------------------------------------------------ backward + update
@@ -343,6 +380,7 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
     pr.arg = li.spec.pool == PST_POOL_MAX2 ? b.arg[slot] : nullptr;
     pr.z = b.z.empty() ? nullptr : b.z[slot];
     pr.relu = li.spec.relu;
+    pr.rscale = li.spec.dropout > 0.f ? drop_scale(li.spec.dropout) : 1.f;
     pr.bn = li.spec.bn;
     pr.y = li.spec.bn ? b.y[slot] : nullptr;
     pr.saved = li.spec.bn ? b.saved[slot] : nullptr;
@@ -415,6 +453,7 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
         c.out = bl.gpre;
         c.bfuse = 1;
         c.brelu = lo.spec.relu;
+        c.bscale = lo.spec.dropout > 0.f ? drop_scale(lo.spec.dropout) : 1.f;
         c.bbn = lo.spec.bn;
         c.bz = bl.z.empty() ? nullptr : bl.z[slot];
         c.by = lo.spec.bn ? bl.y[slot] : nullptr;
@@ -424,7 +463,7 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
       }
       if (li.spec.block_begin && li.block_end >= 0) {
         const LayerInfo& e = net_.layers[li.block_end];
-        c.res = L_[li.block_end - l0].gpre;
+        c.res = li.block_end >= l1 ? dbuf2_[dpar] : L_[li.block_end - l0].gpre;   // mid-block: received
         c.res_mode = e.res_mode;
         c.res_H = e.Ho; c.res_W = e.Wo; c.res_C = e.Coutp; c.res_pad = e.res_pad;
       }

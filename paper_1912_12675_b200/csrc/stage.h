@@ -48,6 +48,18 @@ class Stage {
   act_t* dbuf(int par) const { return dbuf_[par]; }
   size_t input_bytes() const;
   size_t output_bytes() const;
+  // Mid-block register pair (reading AMB-14).  A stage that ENDS inside a residual
+  // block also sends the block input forward and receives the shortcut gradient (the residual
+  // layer's pre-activation gradient) back; a stage that STARTS inside a block receives the block
+  // input and sends its residual layer's pre-activation gradient back.
+  bool ends_mid() const { return end_block_ >= 0; }
+  bool starts_mid() const { return start_res_ >= 0; }
+  act_t* block_out(int slot) const { return in_tensor(end_block_, slot); }   // ends_mid
+  size_t block_out_bytes() const;
+  act_t* input2_slot(int slot) const { return xin2_[slot]; }                 // starts_mid
+  act_t* dbuf2(int par) const { return dbuf2_[par]; }                         // ends_mid
+  act_t* sgrad_out() const { return L_[start_res_ - l0].gpre; }               // starts_mid
+  size_t sgrad_bytes() const;
   float* stage_x() const { return xstage_; }     // stage 0: float NCHW staging of the batch
   size_t stage_x_bytes() const;
   int32_t* label_slot(int64_t mb) const { return label_ring_ + (mb % label_ring_n_) * batch_; }
@@ -81,6 +93,10 @@ class Stage {
   std::vector<LayerBufs> L_;
   std::vector<act_t*> xin_;
   act_t* dbuf_[2] = {nullptr, nullptr};
+  int end_block_ = -1;     // block_begin layer of the block open at the stage's end (-1: none)
+  int start_res_ = -1;     // residual layer closing the block open at the stage's start (-1: none)
+  std::vector<act_t*> xin2_;                     // block input ring (starts_mid)
+  act_t* dbuf2_[2] = {nullptr, nullptr};          // shortcut gradient double buffer (ends_mid)
   float* xstage_ = nullptr;
   float* w_ = nullptr;
   float* v_ = nullptr;
@@ -92,6 +108,10 @@ class Stage {
   int32_t* label_ring_ = nullptr; int label_ring_n_ = 0;
   float* loss_ring_ = nullptr;
   int64_t* fwd_counter_ = nullptr;
+  // dropout
+  bool has_drop_ = false;
+  uint32_t dseed_ = 0;
+  int64_t* d_fmb_ = nullptr;
   float* dz_ = nullptr;
   // optimiser
   SgdSpec sgd_{};

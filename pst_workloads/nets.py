@@ -45,6 +45,7 @@ class LayerSpec:
     residual: bool = False
     relu: bool = False
     pool: str = "none"        # 'none' | 'max2' | 'gap'
+    dropout: float = 0.0      # drop probability, applied after the ReLU (before pooling)
 
     def as_dict(self):
         return asdict(self)
@@ -97,8 +98,12 @@ def alexnet_cifar() -> NetSpec:
     return NetSpec("alexnet", tuple(L), (3, 32, 32), 10)
 
 
-def vgg16_cifar() -> NetSpec:
-    """VGG-16 with BatchNorm for CIFAR-10 (readings AMB-15/16): 16 weighted layers."""
+def vgg16_cifar(dropout: bool = False) -> NetSpec:
+    """VGG-16 with BatchNorm for CIFAR-10 (readings AMB-15/16): 16 weighted layers.
+    dropout=True: "batch normalization and dropout are used during training throughout the
+    network", placed as in the common CIFAR VGG-BN recipe (reading AMB-16b,
+    external): p = 0.3 after the first conv, 0.4 after every other conv not followed by a pool,
+    0.5 after each hidden FC."""
     cfg = [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M"]
     L: List[LayerSpec] = []
     c = 3
@@ -106,11 +111,13 @@ def vgg16_cifar() -> NetSpec:
         if v == "M":
             continue
         pool = "max2" if i + 1 < len(cfg) and cfg[i + 1] == "M" else "none"
-        L.append(conv(c, v, k=3, pad=1, bn=True, relu=True, pool=pool))
+        p = 0.0 if (not dropout or pool != "none") else (0.3 if not L else 0.4)
+        L.append(conv(c, v, k=3, pad=1, bn=True, relu=True, pool=pool, dropout=p))
         c = v
-    L += [fc(512, 512, bias=True, relu=True), fc(512, 512, bias=True, relu=True),
+    q = 0.5 if dropout else 0.0
+    L += [fc(512, 512, bias=True, relu=True, dropout=q), fc(512, 512, bias=True, relu=True, dropout=q),
           fc(512, 10, bias=True)]
-    return NetSpec("vgg16", tuple(L), (3, 32, 32), 10)
+    return NetSpec("vgg16_dropout" if dropout else "vgg16", tuple(L), (3, 32, 32), 10)
 
 
 def resnet_cifar(depth: int) -> NetSpec:
@@ -152,15 +159,16 @@ def tiny_resnet(width: int = 8, hw: int = 8, n: int = 1) -> NetSpec:
     return NetSpec(f"tiny_resnet_w{width}_hw{hw}_n{n}", tuple(L), (3, hw, hw), 10)
 
 
-def tiny_cnn(hw: int = 8) -> NetSpec:
-    """A small LeNet-like net (bias, ReLU, max-pool, FC) for fast tests."""
+def tiny_cnn(hw: int = 8, dropout: float = 0.0) -> NetSpec:
+    """A small LeNet-like net (bias, ReLU, max-pool, FC) for fast tests; `dropout` > 0 puts dropout
+    after the first conv's ReLU (before its pool) and after the hidden FC's ReLU."""
     L = [
-        conv(1, 4, k=3, pad=1, bias=True, relu=True, pool="max2"),
+        conv(1, 4, k=3, pad=1, bias=True, relu=True, pool="max2", dropout=dropout),
         conv(4, 6, k=3, pad=1, bias=True, relu=True, pool="max2"),
-        fc(6 * (hw // 4) * (hw // 4), 12, bias=True, relu=True),
+        fc(6 * (hw // 4) * (hw // 4), 12, bias=True, relu=True, dropout=dropout),
         fc(12, 10, bias=True),
     ]
-    return NetSpec(f"tiny_cnn_hw{hw}", tuple(L), (1, hw, hw), 10)
+    return NetSpec(f"tiny_cnn_hw{hw}" + (f"_do{dropout}" if dropout else ""), tuple(L), (1, hw, hw), 10)
 
 
 def by_name(name: str) -> NetSpec:
@@ -170,6 +178,8 @@ def by_name(name: str) -> NetSpec:
         return alexnet_cifar()
     if name == "vgg16":
         return vgg16_cifar()
+    if name == "vgg16_dropout":
+        return vgg16_cifar(dropout=True)
     if name.startswith("resnet"):
         return resnet_cifar(int(name[len("resnet"):]))
     raise KeyError(name)

@@ -59,14 +59,15 @@ def _test_name():
     return os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0]
 
 
-def oracle_stages(net, ppv):
+def oracle_stages(net, ppv, dropout_seed=0):
     bounds = Net.partition(net.layers, ppv)
-    stages = [Net.CNNStage(net.layers[a:b], first_stage=(s == 0)) for s, (a, b) in enumerate(bounds)]
+    stages = [Net.CNNStage(net.layers[a:b], first_stage=(s == 0), dropout_seed=dropout_seed, layer0=a)
+              for s, (a, b) in enumerate(bounds)]
     return stages, bounds
 
 
-def oracle_run(net, flat, ppv, data, hp, n_p=None, snapshot=False, mom0=None):
-    stages, bounds = oracle_stages(net, ppv)
+def oracle_run(net, flat, ppv, data, hp, n_p=None, snapshot=False, mom0=None, dropout_seed=0):
+    stages, bounds = oracle_stages(net, ppv, dropout_seed)
     per_layer = Net.unflatten(net.layers, flat)
     m0 = None
     if mom0 is not None:
@@ -255,7 +256,7 @@ def compare_final(P, net, ppv, got, got_v, got_bn, losses, ref, deep, sp_final=N
 
 def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, spe=1 << 62,
              milestones=(), per_step=True, seed=5, check=None, deep=False, spread=False, solver_kw=None,
-             tag=None):
+             tag=None, dropout_seed=0):
     """Train the same seeded mini-batches through libpst (all stages on cuda:0, local mode)
     and through Oracle B; compare the weights after every compared step and after the drain
     (split measure, see the module docstring), the momentum buffers and BN running statistics
@@ -274,13 +275,13 @@ def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, sp
     for k, v in skw.items():
         setattr(hp, k, v)
     snap = (True if check is None else set(check)) if per_step else False
-    ref = oracle_run(net, flat, ppv, data, hp, n_p=n_p, snapshot=snap)
+    ref = oracle_run(net, flat, ppv, data, hp, n_p=n_p, snapshot=snap, dropout_seed=dropout_seed)
     P = Parity(tag or _test_name())
     P.ref = ref
     sp_steps, sp_final, sp_mom = {}, None, None
     if spread:
         pert = flat.astype(np.float64) * (1 + 1e-7 * np.random.default_rng(0).standard_normal(flat.shape))
-        refp = oracle_run(net, pert, ppv, data, hp, n_p=n_p, snapshot=snap)
+        refp = oracle_run(net, pert, ppv, data, hp, n_p=n_p, snapshot=snap, dropout_seed=dropout_seed)
         snaps = ref.snapshots if ref.snapshots is not None else {}
         idx = range(len(snaps)) if isinstance(snaps, list) else snaps.keys()
         for t in idx:
@@ -291,7 +292,7 @@ def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, sp
         P.extra["spread_final_where"] = max(sp_final, key=sp_final.get)
         P.extra["k_spread"] = K_SPREAD
     pipe = pst.Pipeline(net, flat, ppv, B, lr, lr_np, momentum=mom, weight_decay=wd, milestones=milestones,
-                        steps_per_epoch=spe, **skw)
+                        steps_per_epoch=spe, dropout_seed=dropout_seed, **skw)
     if n_p is not None:
         assert n_p % spe == 0
         pipe.set_hybrid(n_p // spe)

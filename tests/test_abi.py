@@ -45,7 +45,8 @@ def test_param_count_matches_oracle(pst, name):
 def test_partition_ranges_match_oracle(pst):
     for name, ppvs in [("lenet5", [(1,), (1, 2, 3, 4)]), ("vgg16", [(2, 4, 7), (1, 2, 4, 6, 7, 9, 10)]),
                        ("resnet110", [(37,), (17, 33, 61), (9, 17, 25, 33, 45, 61, 81)]),
-                       ("resnet362", [(121,), (27, 55, 81, 107, 147, 201, 265)])]:
+                       ("resnet362", [(121,), (27, 55, 81, 107, 147, 201, 265)]),
+                       ("resnet20", [(5, 12, 17), (2,), (3, 5, 7, 9, 11, 13, 15, 17, 19)])]:   # mid-block, Table 3
         net = W.by_name(name)
         for ppv in ppvs:
             assert pst.partition_ranges(net, ppv) == Net.partition(net.layers, ppv)
@@ -53,7 +54,7 @@ def test_partition_ranges_match_oracle(pst):
 
 def test_partition_rejections(pst):
     net = W.resnet_cifar(20)
-    for bad, code in [((5, 12, 17), -6), ((7, 7), -1), ((20,), -1), ((0,), -1)]:
+    for bad, code in [((7, 7), -1), ((20,), -1), ((0,), -1), ((5, 4), -1)]:
         with pytest.raises(pst.PstError) as e:
             pst.partition_ranges(net, bad)
         assert e.value.code == code, (bad, e.value)

@@ -143,3 +143,13 @@ def test_resnet20_k4_segments_at_config_lr(pst):
     net = W.nets.by_name("resnet20")
     P = run_segments(pst, net, (7, 13, 19), 32, [10] * 10, [0.01, 0.01, 0.01, 0.1]).assert_ok()
     assert P.ref.losses[-1] < P.ref.losses[0]
+
+
+def test_vgg16_dropout_k4(pst):
+    """configs[2] with the paper's "batch normalization and dropout ... throughout the network"
+    (P:L288): VGG-16-BN with dropout (pst_workloads.vgg16_cifar(dropout=True), reading AMB-16b),
+    4 stages, PPV (2,4,7), batch 64."""
+    net = W.vgg16_cifar(dropout=True)
+    P = run_both(pst, net, W.CONFIGS["vgg16"].ppv[4], 64, 8, [0.001] * 4, mom=0.9, wd=5e-4, check={5, 7},
+                 deep=True, spread=True, dropout_seed=2024).assert_ok()
+    assert list(P.versions) == [8] * 4

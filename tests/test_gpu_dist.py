@@ -148,3 +148,11 @@ def test_dist_k2_resnet110_b128(gpu):
     cfg = W.CONFIGS["resnet110"]
     _check(gpu, dict(net="resnet_cifar", net_kw=dict(depth=110), ppv=list(cfg.ppv[2]), B=128, N=4, seed=31,
                      lr=cfg.lr_vector(2), wd=cfg.weight_decay, deep=True), "dist_k2_resnet110_b128")
+
+
+def test_dist_k3_midblock(gpu):
+    """Mid-block registers over NCCL (reading AMB-14): the block input travels beside the
+    activation and the shortcut gradient beside the input gradient; PPV (2, 6) of a two-block-per-
+    group tiny ResNet splits a plain block and an option-A block.  Then the hybrid switch."""
+    _check(gpu, dict(net="tiny_resnet", net_kw=dict(width=16, hw=8, n=2), ppv=[2, 6], B=32, N=9, seed=27,
+                     lr=[0.02, 0.05, 0.1], lr_np=0.08, n_p=4, spe=2, milestones=[3]), "dist_k3_midblock_hybrid")

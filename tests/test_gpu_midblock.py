@@ -1,0 +1,71 @@
+"""Mid-block pipeline registers and fine-grained PPVs (GPU).
+
+A register pair inside a residual block carries two tensors: the activation and the block input
+forward, the input gradient and the shortcut gradient backward (section 6.3 -- "inserting
+pipeline register pairs within residual function blocks"; section 6.4 -- ResNet-20 with PPV
+(5,12,17), whose 12 sits between the two convolutions of a block; reading AMB-14).  Table 3's
+fine-grained PPVs (3,5,7), (3,5,7,9), ... run too.  Every case is compared with Oracle B
+(whose stages pass the same register pairs, pinned against torch autograd and finite differences in
+tests/test_oracle_pipeline.py) on the same seeded inputs.
+"""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import pst_workloads as W
+from tests.parity import run_both
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pst():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1912_12675_b200 as p
+    return p
+
+
+TINY2 = dict(width=16, hw=8, n=2)   # blocks (2,3) (4,5) (6,7: option-A shortcut) (8,9)
+
+
+@pytest.mark.parametrize("ppv", [(2,), (6,), (2, 4), (1, 2, 3, 6), (2, 4, 6, 8)])
+def test_tiny_resnet_midblock(pst, ppv):
+    net = W.tiny_resnet(**TINY2)
+    K = len(ppv) + 1
+    P = run_both(pst, net, ppv, 32, 10, [0.05] * (K - 1) + [0.1]).assert_ok()
+    assert list(P.versions) == [10] * K
+
+
+def test_tiny_resnet_midblock_hybrid(pst):
+    """Mid-block registers through the hybrid switch (drain, then the non-pipelined exchange)."""
+    net = W.tiny_resnet(**TINY2)
+    P = run_both(pst, net, (2, 6), 32, 9, [0.02, 0.05, 0.1], lr_np=0.08, n_p=4, spe=2,
+                 milestones=(3,)).assert_ok()
+    assert list(P.versions) == [9, 9, 9]
+
+
+def test_resnet20_paper_midblock_ppv(pst):
+    """P:L179's ResNet-20 PPV (5,12,17), four stages, batch 32 at Table 7's stale rate 0.001."""
+    net = W.nets.by_name("resnet20")
+    P = run_both(pst, net, (5, 12, 17), 32, 12, [0.001] * 4, check={6, 11}, deep=True, spread=True).assert_ok()
+    assert list(P.versions) == [12] * 4
+
+
+@pytest.mark.parametrize("ppv", [(3, 5, 7), (3, 5, 7, 9, 11), (3, 5, 7, 9, 11, 13, 15, 17, 19)])
+def test_resnet20_table3_fine_grained(pst, ppv):
+    """Table 3's placements: "8 stages" = PPV (3,5,7), then a register after every 2
+    layers beyond layer 7, up to the paper's "20 stages" (10 GPU stages here, AMB-22)."""
+    net = W.nets.by_name("resnet20")
+    K = len(ppv) + 1
+    N = 2 * K + 2
+    P = run_both(pst, net, ppv, 32, N, [0.001] * K, check={N - 1}, deep=True, spread=True).assert_ok()
+    assert list(P.versions) == [N] * K
+
+
+def test_resnet110_midblock_balance(pst):
+    """A ResNet-110 two-stage split inside a block (layer 48 = the first conv of a group-2 block)
+    at batch 32."""
+    net = W.CONFIGS["resnet110"].netspec()
+    P = run_both(pst, net, (48,), 32, 4, [0.001, 0.001], check={3}, deep=True, spread=True).assert_ok()
+    assert list(P.versions) == [4, 4]

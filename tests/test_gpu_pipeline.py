@@ -139,3 +139,19 @@ def test_abi_error_behaviour(pst):
     pipe.flush()
     assert list(pipe.versions()) == [2]
     pipe.close()
+
+
+@pytest.mark.parametrize("K,ppv", [(1, ()), (2, (1,)), (4, (1, 2, 3))])
+def test_dropout_pipeline(pst, K, ppv):
+    """Dropout (SURVEY f-3; VGG-16's "batch normalization and dropout") with the counter-based
+    masks both sides generate from one definition (pst.h pst_layer.dropout, reading AMB-16b): a conv
+    layer with dropout before its max-pool and a hidden FC with dropout, pipelined."""
+    net = W.tiny_cnn(hw=8, dropout=0.4)
+    P = run_both(pst, net, ppv, 32, 9, [0.05] * K, wd=5e-4, dropout_seed=1234567).assert_ok()
+    assert list(P.versions) == [9] * K
+
+
+def test_dropout_hybrid(pst):
+    net = W.tiny_cnn(hw=8, dropout=0.3)
+    run_both(pst, net, (2,), 32, 9, [0.05, 0.05], lr_np=0.03, n_p=4, spe=2, wd=5e-4,
+             dropout_seed=99).assert_ok()

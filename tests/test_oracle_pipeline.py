@@ -6,7 +6,8 @@ What pins what:
   * version log == closed form max(0, i - 2(K-1-s)) forward / i backward,
   * the hand-derived scalar worked example (tests/golden/scalar_pipeline_k2.json),
   * the K=2 occupancy timeline of P:L61,
-  * Table 1 / Table 5 PPVs valid, Table 4's mid-block (5,12,17) rejected,
+  * Table 1 / Table 5 PPVs valid; mid-block registers (Table 4's (5,12,17)): non-pipelined
+    == torch autograd SGD, pipelined A == B, stage pair == finite differences,
   * Table 6 "Weight" column == 4-byte parameter count in MiB,
   * the speedup formulas of P:L77.
 """
@@ -146,7 +147,7 @@ def test_k2_occupancy_timeline_p61():
 class ScalarStage:
     """h = w * x with params [{'W': w}] -- the net of the worked example."""
 
-    def forward(self, params, x):
+    def forward(self, params, x, mb=0):
         return params[0]["W"] * x, x
 
     def backward(self, params, x, g):
@@ -257,17 +258,114 @@ def test_table1_ppvs_valid(name):
         assert len(Net.partition(net.layers, ppv)) == len(ppv) + 1
 
 
-def test_table5_ppvs_and_midblock_rejection():
+def test_table5_ppvs_and_rejections():
     for depth, p in [(20, 7), (56, 19), (110, 37), (224, 75), (362, 121)]:
         net = W.resnet_cifar(depth)
         assert W.weighted_layer_count(net) == depth
         Net.partition(net.layers, (p,))
-    with pytest.raises(ValueError):
-        Net.partition(W.resnet_cifar(20).layers, (5, 12, 17))
+    assert len(Net.partition(W.resnet_cifar(20).layers, (5, 12, 17))) == 4   # mid-block 12
     with pytest.raises(ValueError):
         Net.partition(W.resnet_cifar(20).layers, (7, 7))
     with pytest.raises(ValueError):
         Net.partition(W.resnet_cifar(20).layers, (20,))
+
+
+def test_midblock_register_positions():
+    """ResNet-20 weighted layers: conv1, then blocks (2,3), (4,5), ..., (18,19), FC 20.  A register
+    after an even layer 2..18 sits inside a block ("inserting pipeline register pairs within
+    residual function blocks"); after an odd one it sits between blocks."""
+    net = W.resnet_cifar(20)
+    opn = Net.open_block_at(net.layers)
+    assert [p for p in range(1, 20) if opn[p]] == list(range(2, 19, 2))
+
+
+MID = {"tiny_resnet2": (W.tiny_resnet(width=4, hw=8, n=2), 6)}
+
+
+@pytest.mark.parametrize("ppv", [(2,), (6,), (2, 4), (1, 2, 4), (2, 3, 6, 8)])
+def test_midblock_nonpipelined_equals_torch_autograd(ppv):
+    """A mid-block partition changes nothing in the arithmetic of non-pipelined training (hybrid
+    with n_p = 0): the two-tensor registers must reproduce torch autograd + torch.optim.SGD over the
+    whole network (library routine, float64) -- a dropped shortcut gradient or a wrong block input
+    fails this."""
+    net, B = MID["tiny_resnet2"]
+    flat = W.init_params(net, seed=13)
+    data = W.batches(net.in_shape, B, 5, seed=17)
+    K = len(ppv) + 1
+    stages, bounds = make_stages(net, ppv)
+    assert any(Net.open_block_at(net.layers)[p] for p in ppv)
+    res = Pl.run_clocked(stages, split_params(net, flat, bounds), data, hp_for(K), n_p=0)
+    t_losses, t_flat = train_sgd(net, flat, data, 0.05, 0.9, 1e-3)
+    np.testing.assert_allclose(res.losses, t_losses, rtol=1e-11, atol=1e-12)
+    np.testing.assert_allclose(flat_of(net, bounds, res.params), t_flat, rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.parametrize("ppv", [(2,), (6,), (2, 4), (1, 2, 3, 4)])
+def test_midblock_versioned_equals_clocked(ppv):
+    """Pipelined with mid-block registers: Oracle A == Oracle B bitwise, versions = closed form."""
+    net, B = MID["tiny_resnet2"]
+    K = len(ppv) + 1
+    flat = W.init_params(net, seed=19)
+    data = W.batches(net.in_shape, B, 9, seed=23)
+    sa, bounds = make_stages(net, ppv)
+    sb, _ = make_stages(net, ppv)
+    p0 = split_params(net, flat, bounds)
+    ra = Pl.run_versioned(sa, p0, data, hp_for(K))
+    rb = Pl.run_clocked(sb, p0, data, hp_for(K))
+    assert ra.losses == rb.losses
+    assert np.array_equal(flat_of(net, bounds, ra.params), flat_of(net, bounds, rb.params))
+    for t, s, kind, mb, ver in rb.version_log:
+        if kind == "F":
+            assert ver == max(0, mb - 2 * (K - 1 - s))
+
+
+def test_midblock_stage_pair_finite_differences():
+    """The backward of a stage pair split inside a block (tuple registers both ways) against
+    central finite differences of the composed loss, for the weights of both stages and the input."""
+    net, B = MID["tiny_resnet2"]
+    ppv = (2,)
+    flat = W.init_params(net, seed=29)
+    x, y = W.make_batch(net.in_shape, B, 0, seed=31)
+    stages, bounds = make_stages(net, ppv)
+    P = split_params(net, flat, bounds)
+    s0, s1 = stages
+    s0.first_stage = False        # also check the input gradient
+
+    def loss_of(P0, P1, xx):
+        st0 = Net.CNNStage(net.layers[bounds[0][0]:bounds[0][1]])
+        st1 = Net.CNNStage(net.layers[bounds[1][0]:bounds[1][1]])
+        h, _ = st0.forward(P0, xx)
+        assert isinstance(h, tuple)
+        o, _ = st1.forward(P1, h)
+        return Lx.softmax_ce(o, y)[0]
+
+    h, c0 = s0.forward(P[0], x)
+    o, c1 = s1.forward(P[1], h)
+    _, g = Lx.softmax_ce(o, y)
+    gh, G1 = s1.backward(P[1], c1, g)
+    assert isinstance(gh, tuple)
+    gx, G0 = s0.backward(P[0], c0, gh)
+    rng = np.random.default_rng(0)
+    eps = 1e-6
+    for st, Pst, G in ((0, P[0], G0), (1, P[1], G1)):
+        for li, d in enumerate(Pst):
+            for k in d:
+                for _ in range(2):
+                    idx = tuple(rng.integers(0, n) for n in d[k].shape)
+                    Pp = [[{kk: v.copy() for kk, v in dd.items()} for dd in ps] for ps in P]
+                    Pm = [[{kk: v.copy() for kk, v in dd.items()} for dd in ps] for ps in P]
+                    Pp[st][li][k][idx] += eps
+                    Pm[st][li][k][idx] -= eps
+                    fd = (loss_of(*Pp, x) - loss_of(*Pm, x)) / (2 * eps)
+                    assert abs(fd - G[li][k][idx]) <= 1e-6 * max(1.0, abs(fd)), (st, li, k, fd, G[li][k][idx])
+    xd = np.asarray(x, dtype=np.float64)
+    for _ in range(3):
+        idx = tuple(rng.integers(0, n) for n in xd.shape)
+        xp, xm = xd.copy(), xd.copy()
+        xp[idx] += eps
+        xm[idx] -= eps
+        fd = (loss_of(P[0], P[1], xp) - loss_of(P[0], P[1], xm)) / (2 * eps)
+        assert abs(fd - gx[idx]) <= 1e-6 * max(1.0, abs(fd))
 
 
 def test_table6_weight_column_param_counts():

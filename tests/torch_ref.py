@@ -18,7 +18,29 @@ def _shapes(L):
     return out
 
 
-def train_sgd(net, flat_params, batches, lr, momentum, weight_decay, lr_fn=None):
+def _fmix32(h):
+    h &= 0xFFFFFFFF
+    h ^= h >> 16
+    h = (h * 0x85EBCA6B) & 0xFFFFFFFF
+    h ^= h >> 13
+    h = (h * 0xC2B2AE35) & 0xFFFFFFFF
+    h ^= h >> 16
+    return h
+
+
+def dropout_mask_py(seed, mb, layer, shape, p):
+    """The counter-based dropout generator of DESIGN.md (reading AMB-16b), written independently of
+    oracle/ with Python integers: key = fmix32(seed ^ fmix32(mb*0x9E3779B9 + (layer+1)*0x632BE5AB)),
+    keep element e iff fmix32(e ^ key) >= floor(float32(p) * 2^32); kept elements scale by 1/(1-p)."""
+    p32 = float(np.float32(p))
+    thr = min(2 ** 32 - 1, int(np.floor(p32 * 2.0 ** 32)))
+    key = _fmix32((seed & 0xFFFFFFFF) ^ _fmix32((mb * 0x9E3779B9 + (layer + 1) * 0x632BE5AB) & 0xFFFFFFFF))
+    n = int(np.prod(shape))
+    keep = [1.0 if _fmix32((e & 0xFFFFFFFF) ^ key) >= thr else 0.0 for e in range(n)]
+    return torch.tensor(keep, dtype=torch.float64).reshape(shape) / (1.0 - p32)
+
+
+def train_sgd(net, flat_params, batches, lr, momentum, weight_decay, lr_fn=None, dropout_seed=0):
     flat = torch.from_numpy(np.asarray(flat_params, dtype=np.float64))
     params, off = [], 0
     for L in net.layers:
@@ -39,7 +61,7 @@ def train_sgd(net, flat_params, batches, lr, momentum, weight_decay, lr_fn=None)
                 g["lr"] = lr_fn(i)
         a = torch.from_numpy(np.asarray(x, dtype=np.float64))
         block_in = None
-        for L, P, R in zip(net.layers, params, running):
+        for li, (L, P, R) in enumerate(zip(net.layers, params, running)):
             if L.block_begin:
                 block_in = a
             if L.kind == "conv":
@@ -57,6 +79,8 @@ def train_sgd(net, flat_params, batches, lr, momentum, weight_decay, lr_fn=None)
                 a = a + sc
             if L.relu:
                 a = F.relu(a)
+            if getattr(L, "dropout", 0.0) > 0.0:
+                a = a * dropout_mask_py(dropout_seed, i, li, tuple(a.shape), L.dropout)
             if L.pool == "max2":
                 a = F.max_pool2d(a, 2, 2)
             elif L.pool == "gap":

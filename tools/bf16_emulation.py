@@ -49,7 +49,7 @@ def R(a):
     return torch.from_numpy(np.asarray(a, dtype=np.float64)).to(DT).double().numpy()
 
 class EmuStage(Net.CNNStage):
-    def forward(self, params, x):
+    def forward(self, params, x, mb=0):
         a = R(x)
         caches, block_in = [], None
         for L, P, S in zip(self.layers, params, self.state):
