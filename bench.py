@@ -148,6 +148,49 @@ def blas_threads():
         return os.cpu_count()
 
 
+def oracle_lenet5_config(n_steps=20):
+    """BASELINE configs[0] in full through the oracle's schedule: LeNet-5, MNIST-shaped, batch 64,
+    2 stages (PPV (1)), n_steps mini-batches (Oracle B, fill and drain included); img/s."""
+    import pst_workloads as W
+    from oracle import network as Net, pipeline as Pl
+    cfg = W.CONFIGS["lenet5"]
+    net = cfg.netspec()
+    flat = W.init_params(net, seed=42)
+    bounds = Net.partition(net.layers, cfg.ppv[2])
+    st = [Net.CNNStage(net.layers[a:b], first_stage=(s == 0), layer0=a) for s, (a, b) in enumerate(bounds)]
+    per = Net.unflatten(net.layers, flat)
+    hp = Pl.HParams(lr_pipelined=cfg.lr_vector(2), lr_nonpipelined=cfg.base_lr, momentum=cfg.momentum,
+                    weight_decay=cfg.weight_decay)
+    data = [W.make_batch(net.in_shape, cfg.batch, i, seed=1234) for i in range(n_steps)]
+    t0 = time.perf_counter()
+    Pl.run_clocked(st, [per[a:b] for a, b in bounds], data, hp)
+    dt = time.perf_counter() - t0
+    return n_steps * cfg.batch / dt, dt
+
+
+def cpu_baseline(cfg, sample):
+    """SURVEY 8(d) oracle timing: the bench workload (one non-pipelined SGD step of the full
+    batch-128 mini-batch, fp64 NumPy, BLAS threads = host cores) as `value`; beside it the same step
+    on a `sample`-image slice with ONE BLAS thread, and BASELINE configs[0] (LeNet-5 K=2, 20 steps) in
+    full.  About 20-40 s of host time."""
+    rate, dt = oracle_sample_rate(cfg, cfg.batch, 1)
+    out = {"value": rate, "unit": "img/s", "cores": blas_threads(), "kind": "oracle",
+           "host_cpus": os.cpu_count(),
+           "sample": f"1 non-pipelined SGD step of {cfg.net} on a full {cfg.batch}-image mini-batch "
+                     f"({dt:.1f} s, float64 NumPy, BLAS threads = {blas_threads()})"}
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1, user_api="blas"):
+            r1, d1 = oracle_sample_rate(cfg, sample, 1)
+        out["one_thread"] = {"value": r1, "unit": "img/s", "sample": f"{sample}-image slice, 1 BLAS thread ({d1:.1f} s)"}
+    except Exception as e:   # threadpoolctl missing: report, do not fail the bench
+        out["one_thread"] = {"unavailable": str(e)[:120]}
+    rl, dl = oracle_lenet5_config(20)
+    out["lenet5_k2_config0"] = {"value": rl, "unit": "img/s", "seconds": dl,
+                                "sample": "BASELINE configs[0] in full: LeNet-5 b64, 2 stages, 20 steps (Oracle B)"}
+    return out
+
+
 def run_reference(args, rank, world):
     import pst_workloads as W
     if rank != 0:
@@ -370,13 +413,26 @@ def main():
         e2e = {"value": args.steps * B / dt, "unit": "img/s",
                "h2d_bytes_per_step": int(host[0][0].nbytes + host[0][1].nbytes), "d2h_bytes_per_step": 4}
 
+    # ---- per-stage device memory (pst_memory; the paper's activation storage P:L65/L75, Table 6)
+    mine = [dict(stage=s_, **pipe.memory(s_)) for s_ in ([my_stage] if world > 1 else range(K))]
+    if dist is not None:
+        allm = [None] * world
+        dist.all_gather_object(allm, mine)
+        mine = [m for part in allm for m in part]
+    memory = {"per_stage": mine,
+              "note": "bytes_per_slot = saved forward state of one mini-batch; ring_slots kept vs the paper's "
+                      "2(K-s)-1 (paper_slots); total = every device buffer of the stage"}
+    tot = sum(m["bytes_per_slot"] for m in mine)
+    extra_paper = sum((m["paper_slots"] - 1) * m["bytes_per_slot"] for m in mine)
+    extra_kept = sum((m["ring_slots"] - 1) * m["bytes_per_slot"] for m in mine)
+    pbytes = sum(m["param_bytes"] for m in mine)
+    memory["increase_pct_paper_depth"] = 100.0 * extra_paper / (tot + pbytes) if tot else None
+    memory["increase_pct_as_built"] = 100.0 * extra_kept / (tot + pbytes) if tot else None
+
     # ---- CPU oracle baseline (rank 0, N == 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, dt = oracle_sample_rate(cfg, args.cpu_sample, 1)
-        cpu = {"value": rate, "unit": "img/s", "cores": blas_threads(), "kind": "oracle",
-               "sample": f"1 non-pipelined SGD step of {cfg.net} on a {args.cpu_sample}-image slice "
-                         f"({dt:.1f} s, float64 NumPy)"}
+        cpu = cpu_baseline(cfg, args.cpu_sample)
 
     if rank == 0:
         line = {
@@ -391,7 +447,7 @@ def main():
                        "lr_per_stage": lr},
             "clocks": clk, "gpu_launches": launches, "roofline": roofline, "conv_tensor_pipe": conv_pipe,
             "kernels": kernel_table,
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "memory": memory,
             "paper_context": {"img_s_1gpu_gtx1060": 760, "img_s_2gpu_gtx1060": 1321, "source": "PAPER.md L192"},
         }
         print(json.dumps(line), flush=True)

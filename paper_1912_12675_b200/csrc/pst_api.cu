@@ -167,7 +167,7 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
         const int ds = (int)(prev_stage.fwd_mb % S->R);
         PST_NCCL(ncclRecv(S->input_slot(ds), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
         if (S->starts_mid())
-          PST_NCCL(ncclRecv(S->input2_slot(ds), S->block_out_bytes(), ncclUint8, s - 1, c->comm, st));
+          PST_NCCL(ncclRecv(S->input2_slot(ds), S->input2_bytes(), ncclUint8, s - 1, c->comm, st));
       }
       if (send_b) {
         PST_NCCL(ncclSend(S->dgrad_out(), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
@@ -176,7 +176,7 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
       if (recv_b) {
         const int par = (int)(next_stage.bwd_mb & 1);
         PST_NCCL(ncclRecv(S->dbuf(par), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
-        if (S->ends_mid()) PST_NCCL(ncclRecv(S->dbuf2(par), S->sgrad_bytes(), ncclUint8, s + 1, c->comm, st));
+        if (S->ends_mid()) PST_NCCL(ncclRecv(S->dbuf2(par), S->dbuf2_bytes(), ncclUint8, s + 1, c->comm, st));
       }
       PST_NCCL(ncclGroupEnd());
     }
@@ -193,7 +193,7 @@ static void enqueue_np(pst_ctx* c, int s, int64_t i, bool fwd, cudaStream_t st) 
     if (c->dist && s > 0) {
       PST_NCCL(ncclGroupStart());
       PST_NCCL(ncclRecv(S->input_slot(slot), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
-      if (S->starts_mid()) PST_NCCL(ncclRecv(S->input2_slot(slot), S->block_out_bytes(), ncclUint8, s - 1, c->comm, st));
+      if (S->starts_mid()) PST_NCCL(ncclRecv(S->input2_slot(slot), S->input2_bytes(), ncclUint8, s - 1, c->comm, st));
       PST_NCCL(ncclGroupEnd());
     }
     S->enqueue_forward(slot, st);
@@ -215,7 +215,7 @@ static void enqueue_np(pst_ctx* c, int s, int64_t i, bool fwd, cudaStream_t st) 
     if (c->dist && s < K - 1) {
       PST_NCCL(ncclGroupStart());
       PST_NCCL(ncclRecv(S->dbuf(par), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
-      if (S->ends_mid()) PST_NCCL(ncclRecv(S->dbuf2(par), S->sgrad_bytes(), ncclUint8, s + 1, c->comm, st));
+      if (S->ends_mid()) PST_NCCL(ncclRecv(S->dbuf2(par), S->dbuf2_bytes(), ncclUint8, s + 1, c->comm, st));
       PST_NCCL(ncclGroupEnd());
     }
     S->enqueue_backward(slot, par, st);

@@ -140,8 +140,8 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     dbuf_[0] = alloc<act_t>(ob);
     dbuf_[1] = alloc<act_t>(ob);
     if (ends_mid()) {
-      dbuf2_[0] = alloc<act_t>(sgrad_bytes() / sizeof(act_t));
-      dbuf2_[1] = alloc<act_t>(sgrad_bytes() / sizeof(act_t));
+      dbuf2_[0] = alloc<act_t>(dbuf2_bytes() / sizeof(act_t));
+      dbuf2_[1] = alloc<act_t>(dbuf2_bytes() / sizeof(act_t));
     }
   } else {
     label_ring_n_ = 2 * K + 2;
@@ -271,14 +271,20 @@ size_t Stage::output_bytes() const {
   const LayerInfo& li = net_.layers[l1 - 1];
   return (size_t)batch_ * li.out_H * li.out_W * ((li.out_C + 15) / 16 * 16) * sizeof(act_t);
 }
-size_t Stage::block_out_bytes() const {   // the block input of the block open at the stage's end
-  const LayerInfo& src = net_.layers[end_block_ >= 0 ? end_block_ : net_.layers[start_res_].block_src];
-  return (size_t)batch_ * src.in_H * src.in_W * src.in_Cp * sizeof(act_t);
+// Mid-block register sizes.  A stage may both start and end inside (different) blocks, so the
+// sent and the received tensors of each direction are sized from their own block.
+static size_t block_input_bytes(const NetInfo& net, int block_begin, int B) {   // the block's input
+  const LayerInfo& src = net.layers[block_begin];
+  return (size_t)B * src.in_H * src.in_W * src.in_Cp * sizeof(act_t);
 }
-size_t Stage::sgrad_bytes() const {        // the closing residual layer's pre-activation gradient
-  const LayerInfo& e = net_.layers[start_res_ >= 0 ? start_res_ : net_.layers[end_block_].block_end];
-  return (size_t)batch_ * e.Ho * e.Wo * e.Coutp * sizeof(act_t);
+static size_t residual_grad_bytes(const NetInfo& net, int residual, int B) {   // its pre-activation gradient
+  const LayerInfo& e = net.layers[residual];
+  return (size_t)B * e.Ho * e.Wo * e.Coutp * sizeof(act_t);
 }
+size_t Stage::block_out_bytes() const { return block_input_bytes(net_, end_block_, batch_); }
+size_t Stage::dbuf2_bytes() const { return residual_grad_bytes(net_, net_.layers[end_block_].block_end, batch_); }
+size_t Stage::input2_bytes() const { return block_input_bytes(net_, net_.layers[start_res_].block_src, batch_); }
+size_t Stage::sgrad_bytes() const { return residual_grad_bytes(net_, start_res_, batch_); }
 size_t Stage::stage_x_bytes() const {
   return (size_t)batch_ * net_.in_C * net_.in_H * net_.in_W * sizeof(float);
 }

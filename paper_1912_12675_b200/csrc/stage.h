@@ -54,11 +54,13 @@ class Stage {
   // input and sends its residual layer's pre-activation gradient back.
   bool ends_mid() const { return end_block_ >= 0; }
   bool starts_mid() const { return start_res_ >= 0; }
-  act_t* block_out(int slot) const { return in_tensor(end_block_, slot); }   // ends_mid
+  act_t* block_out(int slot) const { return in_tensor(end_block_, slot); }   // ends_mid: sent forward
   size_t block_out_bytes() const;
-  act_t* input2_slot(int slot) const { return xin2_[slot]; }                 // starts_mid
-  act_t* dbuf2(int par) const { return dbuf2_[par]; }                         // ends_mid
-  act_t* sgrad_out() const { return L_[start_res_ - l0].gpre; }               // starts_mid
+  act_t* dbuf2(int par) const { return dbuf2_[par]; }                         // ends_mid: received
+  size_t dbuf2_bytes() const;
+  act_t* input2_slot(int slot) const { return xin2_[slot]; }                 // starts_mid: received
+  size_t input2_bytes() const;
+  act_t* sgrad_out() const { return L_[start_res_ - l0].gpre; }               // starts_mid: sent back
   size_t sgrad_bytes() const;
   float* stage_x() const { return xstage_; }     // stage 0: float NCHW staging of the batch
   size_t stage_x_bytes() const;

@@ -28,7 +28,8 @@ torch = pytest.importorskip("torch")
 
 import pst_workloads as W
 from oracle import network as Net
-from tests.parity import Parity, compare_final, hparams, oracle_run
+from tests.parity import (K_EMU, K_SPREAD, Parity, allowances, compare_final, hparams, oracle_run, oracle_spreads,
+                          perturbed)
 
 pytestmark = pytest.mark.gpu
 
@@ -102,6 +103,9 @@ def _check(gpu, case, tag):
     hp = hparams(case["lr"], K, case.get("lr_np", case["lr"][-1]), case.get("mom", 0.9), case.get("wd", 1e-4),
                  case.get("milestones", ()), 0.1, case.get("spe", 1 << 62))
     ref = oracle_run(net, flat, ppv, data, hp, n_p=case.get("n_p"))
+    sp_p = oracle_spreads(net, ppv, ref, oracle_run(net, perturbed(flat), ppv, data, hp, n_p=case.get("n_p")))
+    sp_e = oracle_spreads(net, ppv, ref, oracle_run(net, flat, ppv, data, hp, n_p=case.get("n_p"), emu=True))
+    sp = allowances(sp_p, sp_e)
     got, work = _launch(case)
     for s in range(K):
         assert list(got[s]["versions"]) == [case["N"]], (s, got[s]["versions"])
@@ -110,7 +114,9 @@ def _check(gpu, case, tag):
     g_v = np.concatenate([g["momentum"] for g in got])
     g_bn = np.concatenate([g["bnstats"] for g in got])
     P = Parity(tag)
-    compare_final(P, net, ppv, g_p, g_v, g_bn, got[K - 1]["losses"], ref, deep=case.get("deep", False))
+    compare_final(P, net, ppv, g_p, g_v, g_bn, got[K - 1]["losses"], ref, deep=case.get("deep", False), sp=sp)
+    P.extra.update(spread_final_max=max(sp_p["w"].values()), emu_dev_momentum_max=max(sp_e["vs"].values()),
+                   k_spread=K_SPREAD, k_emu=K_EMU)
     # distributed vs local mode on the same GPU: same kernels, same inputs
     loc, loc_loss = _local(gpu, case, net, flat, data)
     mine = np.concatenate([g_p, g_v, g_bn])
@@ -125,14 +131,14 @@ def _check(gpu, case, tag):
 def test_dist_k2_tiny_resnet(gpu):
     """Two ranks, PPV (3): pipelined fill, steady state and drain over NCCL."""
     _check(gpu, dict(net="tiny_resnet", net_kw=dict(width=16, hw=8, n=1), ppv=[3], B=32, N=8, seed=21,
-                lr=[0.05, 0.1]), "dist_k2_tiny_resnet")
+                lr=[0.05, 0.1], deep=True), "dist_k2_tiny_resnet")
 
 
 def test_dist_k3_hybrid(gpu):
     """Three ranks with the hybrid switch (reading AMB-10): pipelined for 4 mini-batches,
     drain, then the non-pipelined exchange (ungrouped send/recv per mini-batch), lr milestone."""
     _check(gpu, dict(net="tiny_resnet", net_kw=dict(width=16, hw=8, n=1), ppv=[1, 3], B=32, N=9, seed=23,
-                lr=[0.02, 0.05, 0.1], lr_np=0.08, n_p=4, spe=2, milestones=[3]), "dist_k3_hybrid")
+                lr=[0.02, 0.05, 0.1], lr_np=0.08, n_p=4, spe=2, milestones=[3], deep=True), "dist_k3_hybrid")
 
 
 def test_dist_k4_tiny_cnn(gpu):
@@ -155,4 +161,5 @@ def test_dist_k3_midblock(gpu):
     activation and the shortcut gradient beside the input gradient; PPV (2, 6) of a two-block-per-
     group tiny ResNet splits a plain block and an option-A block.  Then the hybrid switch."""
     _check(gpu, dict(net="tiny_resnet", net_kw=dict(width=16, hw=8, n=2), ppv=[2, 6], B=32, N=9, seed=27,
-                     lr=[0.02, 0.05, 0.1], lr_np=0.08, n_p=4, spe=2, milestones=[3]), "dist_k3_midblock_hybrid")
+                     lr=[0.002, 0.005, 0.01], lr_np=0.008, n_p=4, spe=2, milestones=[3], deep=True),
+           "dist_k3_midblock_hybrid")

@@ -27,21 +27,27 @@ def pst():
 
 
 TINY2 = dict(width=16, hw=8, n=2)   # blocks (2,3) (4,5) (6,7: option-A shortcut) (8,9)
+# This net's second group runs at 4x4: a ReLU pre-activation within float32 rounding of 0 that takes
+# the other side moves 1/512 of a channel's gradient, so even the float32-emulated oracle jumps by
+# up to 2.4e-3 per tensor at lr 0.05-0.1 over 10 steps (tools/flip_probe.py).  The weight update
+# scales that by lr: these structural tests run at lr 0.005/0.01 (a lost shortcut gradient or a
+# wrong block input still moves the weights by O(lr * |g|), ~10x the tolerance) and the momentum
+# buffers (lr-independent) carry the gradient check (reading AMB-21f).
 
 
 @pytest.mark.parametrize("ppv", [(2,), (6,), (2, 4), (1, 2, 3, 6), (2, 4, 6, 8)])
 def test_tiny_resnet_midblock(pst, ppv):
     net = W.tiny_resnet(**TINY2)
     K = len(ppv) + 1
-    P = run_both(pst, net, ppv, 32, 10, [0.05] * (K - 1) + [0.1]).assert_ok()
+    P = run_both(pst, net, ppv, 32, 10, [0.005] * (K - 1) + [0.01], deep=True).assert_ok()
     assert list(P.versions) == [10] * K
 
 
 def test_tiny_resnet_midblock_hybrid(pst):
     """Mid-block registers through the hybrid switch (drain, then the non-pipelined exchange)."""
     net = W.tiny_resnet(**TINY2)
-    P = run_both(pst, net, (2, 6), 32, 9, [0.02, 0.05, 0.1], lr_np=0.08, n_p=4, spe=2,
-                 milestones=(3,)).assert_ok()
+    P = run_both(pst, net, (2, 6), 32, 9, [0.002, 0.005, 0.01], lr_np=0.008, n_p=4, spe=2,
+                 milestones=(3,), deep=True).assert_ok()
     assert list(P.versions) == [9, 9, 9]
 
 
