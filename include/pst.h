@@ -232,11 +232,12 @@ int pst_stage_times(pst_ctx* ctx, double* ms, int32_t cap, int64_t* steps);
 /* Device memory of an owned stage (the paper's memory analysis, section 3 and Table 6
  * P:L198-212 section 6.6: a stage keeps the activations of 2(K-s)-1 mini-batches).  out[cap >= 5]:
  *   out[0] device bytes the stage allocated (all buffers);
- *   out[1] saved-activation ring slots R_s this build keeps (2(K-s)+1 rounded up to a divisor of
- *          2K+2, model.h ring_slots);
+ *   out[1] saved-activation ring slots R_s this build keeps (2(K-s)-1 rounded up to a divisor of
+ *          2K+2, model.h ring_saved);
  *   out[2] the paper's count 2(K-s)-1;
  *   out[3] bytes of the saved forward state of one mini-batch (one slot);
- *   out[4] bytes of the stage's parameters (one float32 copy). */
+ *   out[4] bytes of the stage's parameters (one float32 copy);
+ *   out[5] (cap >= 6) input-ring slots (2(K-s)+1 for s > 0 rounded likewise, model.h ring_input). */
 int pst_memory(pst_ctx* ctx, int32_t stage, int64_t* out, int32_t cap);
 
 void pst_destroy(pst_ctx* ctx);

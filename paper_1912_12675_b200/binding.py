@@ -283,10 +283,10 @@ class Pipeline:
 
     def memory(self, stage: int) -> dict:
         """Device memory of an owned stage (pst_memory)."""
-        out = (C.c_int64 * 5)()
-        self._c(lib().pst_memory(self._ctx, stage, out, 5))
+        out = (C.c_int64 * 6)()
+        self._c(lib().pst_memory(self._ctx, stage, out, 6))
         return {"bytes_total": out[0], "ring_slots": out[1], "paper_slots": out[2], "bytes_per_slot": out[3],
-                "param_bytes": out[4]}
+                "param_bytes": out[4], "input_ring_slots": out[5]}
 
     def launches(self) -> int:
         n = C.c_int64()

@@ -57,22 +57,24 @@ std::vector<std::pair<int, int>> partition(const NetInfo& net, int K, const int3
 struct StepPlan { int64_t bwd_mb = -1, fwd_mb = -1; };
 StepPlan plan_step(int K, int s, int64_t t, int64_t t0, int64_t m0, int64_t n_fed);
 
-// Saved-activation / input ring slots per stage.  Stage s keeps the saved forward state of the
-// mini-batches between its forward (step f+s) and its backward (step f+2K-1-s): 2(K-s)-1 of them
-// right after a forward (the paper's activation storage), plus 2 so a forward never
-// overwrites an input slot the neighbour's copy of the same step is writing or an in-flight read
-// still needs: need_s = 2(K-s)+1.  Every R_s is a divisor of one common period P = 2K+2 (the
-// smallest divisor >= need_s), so all ring indices and the gradient-buffer parity cycle with
-// period P and a stage needs at most P distinct step graphs (arbitrary per-stage sizes 2(K-s)+1
-// would make the graph key cycle with lcm(2, R_s, R_{s+1}): 6630 step graphs for the second stage
-// of an 8-stage pipeline).  K=8: 18,18,18,18,9,9,6,3 slots instead of 18 on every stage.
-inline int ring_need(int K, int s) { return 2 * (K - s) + 1; }
+// Ring sizes of stage s (K stages).  The saved forward state of a mini-batch lives from its forward
+// (step f+s) to its backward (step f+2K-1-s); the backward of a step runs before its forward on the
+// same stream, so 2(K-s)-1 slots hold it -- the paper's activation storage (section 3;
+// Table 6).  A stage s > 0 also keeps an input ring that its neighbour's copy of mini-batch
+// f+1 writes while the stage still reads the inputs of b..f in the same step: 2(K-s)+1 slots.  Every
+// ring size is rounded up to a divisor of one common period P = 2K+2, so all ring indices and the
+// gradient-buffer parity cycle with period P and a stage needs at most P distinct step graphs (sizes
+// 2(K-s)-1 / 2(K-s)+1 as they are would make the graph key cycle with their lcm: 6630 step graphs for
+// the second stage of an 8-stage pipeline).  K=8 saved-state slots: 18,18,18,9,9,6,3,1 (paper:
+// 15,13,11,9,7,5,3,1).
 inline int ring_period(int K) { return 2 * K + 2; }
-inline int ring_slots(int K, int s) {
-  const int P = ring_period(K), need = ring_need(K, s);
+inline int ring_divisor_at_least(int K, int need) {
+  const int P = ring_period(K);
   for (int d = need; d < P; ++d)
     if (P % d == 0) return d;
   return P;
 }
+inline int ring_saved(int K, int s) { return ring_divisor_at_least(K, 2 * (K - s) - 1); }
+inline int ring_input(int K, int s) { return s == 0 ? ring_saved(K, 0) : ring_divisor_at_least(K, 2 * (K - s) + 1); }
 
 }  // namespace pst

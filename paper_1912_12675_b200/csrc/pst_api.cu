@@ -132,7 +132,7 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
   Stage* S = c->stage(s);
   const int K = c->K;
   if (p.bwd_mb >= 0) {
-    S->enqueue_backward((int)(p.bwd_mb % S->R), (int)(p.bwd_mb & 1), st);
+    S->enqueue_backward(p.bwd_mb, (int)(p.bwd_mb & 1), st);
     if (s > 0 && !c->dist) {
       Stage* D = c->stage(s - 1);
       const int par = (int)(p.bwd_mb & 1);
@@ -142,13 +142,13 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
     }
   }
   if (p.fwd_mb >= 0) {
-    S->enqueue_forward((int)(p.fwd_mb % S->R), st);
+    S->enqueue_forward(p.fwd_mb, st);
     if (s < K - 1 && !c->dist) {
       Stage* D = c->stage(s + 1);
-      const int ss = (int)(p.fwd_mb % S->R), ds = (int)(p.fwd_mb % D->R);
-      PST_CUDA(cudaMemcpyAsync(D->input_slot(ds), S->output_slot(ss), S->output_bytes(), cudaMemcpyDefault, st));
+      const int64_t f = p.fwd_mb;
+      PST_CUDA(cudaMemcpyAsync(D->input_slot(f), S->output_slot(f), S->output_bytes(), cudaMemcpyDefault, st));
       if (S->ends_mid())     // mid-block register: the block input goes forward too
-        PST_CUDA(cudaMemcpyAsync(D->input2_slot(ds), S->block_out(ss), S->block_out_bytes(), cudaMemcpyDefault, st));
+        PST_CUDA(cudaMemcpyAsync(D->input2_slot(f), S->block_out(f), S->block_out_bytes(), cudaMemcpyDefault, st));
     }
   }
   if (c->dist) {
@@ -159,15 +159,15 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
     if (send_f || recv_f || send_b || recv_b) {
       PST_NCCL(ncclGroupStart());
       if (send_f) {
-        const int ss = (int)(p.fwd_mb % S->R);
-        PST_NCCL(ncclSend(S->output_slot(ss), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
-        if (S->ends_mid()) PST_NCCL(ncclSend(S->block_out(ss), S->block_out_bytes(), ncclUint8, s + 1, c->comm, st));
+        const int64_t f = p.fwd_mb;
+        PST_NCCL(ncclSend(S->output_slot(f), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+        if (S->ends_mid()) PST_NCCL(ncclSend(S->block_out(f), S->block_out_bytes(), ncclUint8, s + 1, c->comm, st));
       }
       if (recv_f) {
-        const int ds = (int)(prev_stage.fwd_mb % S->R);
-        PST_NCCL(ncclRecv(S->input_slot(ds), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
+        const int64_t f = prev_stage.fwd_mb;
+        PST_NCCL(ncclRecv(S->input_slot(f), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
         if (S->starts_mid())
-          PST_NCCL(ncclRecv(S->input2_slot(ds), S->input2_bytes(), ncclUint8, s - 1, c->comm, st));
+          PST_NCCL(ncclRecv(S->input2_slot(f), S->input2_bytes(), ncclUint8, s - 1, c->comm, st));
       }
       if (send_b) {
         PST_NCCL(ncclSend(S->dgrad_out(), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
@@ -187,28 +187,26 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
 static void enqueue_np(pst_ctx* c, int s, int64_t i, bool fwd, cudaStream_t st) {
   Stage* S = c->stage(s);
   const int K = c->K;
-  const int slot = (int)(i % S->R);
   const int par = (int)(i & 1);
   if (fwd) {
     if (c->dist && s > 0) {
       PST_NCCL(ncclGroupStart());
-      PST_NCCL(ncclRecv(S->input_slot(slot), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
-      if (S->starts_mid()) PST_NCCL(ncclRecv(S->input2_slot(slot), S->input2_bytes(), ncclUint8, s - 1, c->comm, st));
+      PST_NCCL(ncclRecv(S->input_slot(i), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
+      if (S->starts_mid()) PST_NCCL(ncclRecv(S->input2_slot(i), S->input2_bytes(), ncclUint8, s - 1, c->comm, st));
       PST_NCCL(ncclGroupEnd());
     }
-    S->enqueue_forward(slot, st);
+    S->enqueue_forward(i, st);
     if (s < K - 1) {
       if (c->dist) {
         PST_NCCL(ncclGroupStart());
-        PST_NCCL(ncclSend(S->output_slot(slot), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
-        if (S->ends_mid()) PST_NCCL(ncclSend(S->block_out(slot), S->block_out_bytes(), ncclUint8, s + 1, c->comm, st));
+        PST_NCCL(ncclSend(S->output_slot(i), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
+        if (S->ends_mid()) PST_NCCL(ncclSend(S->block_out(i), S->block_out_bytes(), ncclUint8, s + 1, c->comm, st));
         PST_NCCL(ncclGroupEnd());
       } else {
         Stage* D = c->stage(s + 1);
-        const int ds = (int)(i % D->R);
-        PST_CUDA(cudaMemcpyAsync(D->input_slot(ds), S->output_slot(slot), S->output_bytes(), cudaMemcpyDefault, st));
+        PST_CUDA(cudaMemcpyAsync(D->input_slot(i), S->output_slot(i), S->output_bytes(), cudaMemcpyDefault, st));
         if (S->ends_mid())
-          PST_CUDA(cudaMemcpyAsync(D->input2_slot(ds), S->block_out(slot), S->block_out_bytes(), cudaMemcpyDefault, st));
+          PST_CUDA(cudaMemcpyAsync(D->input2_slot(i), S->block_out(i), S->block_out_bytes(), cudaMemcpyDefault, st));
       }
     }
   } else {
@@ -218,7 +216,7 @@ static void enqueue_np(pst_ctx* c, int s, int64_t i, bool fwd, cudaStream_t st) 
       if (S->ends_mid()) PST_NCCL(ncclRecv(S->dbuf2(par), S->dbuf2_bytes(), ncclUint8, s + 1, c->comm, st));
       PST_NCCL(ncclGroupEnd());
     }
-    S->enqueue_backward(slot, par, st);
+    S->enqueue_backward(i, par, st);
     if (s > 0) {
       if (c->dist) {
         PST_NCCL(ncclGroupStart());
@@ -295,12 +293,13 @@ static void pipe_step(pst_ctx* c) {
     const StepPlan next = s < K - 1 ? plans[s + 1] : StepPlan{};
     Stage* S = c->stage(s);
     GraphKey key;
-    auto slot = [](int64_t mb, int R) { return mb >= 0 ? mb % R : -1; };
-    key.k = {0, slot(p.bwd_mb, S->R), p.bwd_mb >= 0 ? (p.bwd_mb & 1) : -1, slot(p.fwd_mb, S->R),
-             s < K - 1 && p.fwd_mb >= 0 ? p.fwd_mb % ring_slots(K, s + 1) : -1,
-             s > 0 && prev.fwd_mb >= 0 ? slot(prev.fwd_mb, S->R) : -1,
+    // every ring size divides P (model.h), so the buffers a step program touches are functions of
+    // its mini-batch indices mod P (P even: parities too)
+    const int64_t P = ring_period(K);
+    auto m = [P](int64_t mb) { return mb >= 0 ? mb % P : -1; };
+    key.k = {0, m(p.bwd_mb), m(p.fwd_mb), s > 0 ? m(prev.fwd_mb) : -1,
              s < K - 1 && next.bwd_mb >= 0 ? (next.bwd_mb & 1) : -1};
-    if (p.bwd_mb < 0 && p.fwd_mb < 0 && key.k[5] < 0 && key.k[6] < 0) continue;
+    if (p.bwd_mb < 0 && p.fwd_mb < 0 && key.k[3] < 0 && key.k[4] < 0) continue;
     const int li = c->local_index(s);
     if (c->stage_timing) {
       if (!c->dist && s > 0) PST_CUDA(cudaStreamWaitEvent(S->stream, c->st_end[s - 1], 0));
@@ -353,7 +352,7 @@ static void np_step(pst_ctx* c) {
       PST_CUDA(cudaStreamWaitEvent(S->stream, c->done[s - 1], 0));
     }
     GraphKey key;
-    key.k = {1, i % S->R};
+    key.k = {1, i % ring_period(K)};
     run_program(c, s, key, [&](cudaStream_t st) { enqueue_np(c, s, i, true, st); });
     PST_CUDA(cudaEventRecord(c->done[c->local_index(s)], S->stream));
   }
@@ -365,7 +364,7 @@ static void np_step(pst_ctx* c) {
       PST_CUDA(cudaStreamWaitEvent(S->stream, c->done[s + 1], 0));
     }
     GraphKey key;
-    key.k = {2, i % S->R, i & 1};
+    key.k = {2, i % ring_period(K)};
     run_program(c, s, key, [&](cudaStream_t st) { enqueue_np(c, s, i, false, st); });
     PST_CUDA(cudaEventRecord(c->done[c->local_index(s)], S->stream));
   }
@@ -776,6 +775,7 @@ int pst_memory(pst_ctx* c, int32_t stage, int64_t* out, int32_t cap) {
     out[0] = (int64_t)S->bytes_total;
     out[1] = S->R;
     out[2] = 2 * (c->K - stage) - 1;
+    if (cap >= 6) out[5] = S->Rin;
     out[3] = (int64_t)S->bytes_slot;
     out[4] = S->n_params * (int64_t)sizeof(float);
   });

@@ -43,7 +43,8 @@ T* Stage::alloc(size_t n, bool zero) {
 
 Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, const pst_hparams& hp,
              const float* init_params, int batch)
-    : s(s_), K(K_), l0(l0_), l1(l1_), dev(device), R(ring_slots(K_, s_)), batch_(batch), net_(net) {
+    : s(s_), K(K_), l0(l0_), l1(l1_), dev(device), R(ring_saved(K_, s_)), Rin(ring_input(K_, s_)), batch_(batch),
+      net_(net) {
   PST_CUDA(cudaSetDevice(dev));
   PST_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   PST_CUDA(cudaStreamCreateWithFlags(&wstream, cudaStreamNonBlocking));
@@ -67,11 +68,11 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     if (net.layers[l].spec.block_begin && net.layers[l].block_end >= l1) end_block_ = l;
   // input ring of the stage
   const LayerInfo& f0 = net.layers[l0];
-  for (int r = 0; r < R; ++r) xin_.push_back(alloc<act_t>((size_t)B * f0.in_H * f0.in_W * f0.in_Cp));
+  for (int r = 0; r < Rin; ++r) xin_.push_back(alloc<act_t>((size_t)B * f0.in_H * f0.in_W * f0.in_Cp));
   bytes_slot += (size_t)B * f0.in_H * f0.in_W * f0.in_Cp * sizeof(act_t);
   if (starts_mid()) {
     const LayerInfo& src = net.layers[net.layers[start_res_].block_src];
-    for (int r = 0; r < R; ++r) xin2_.push_back(alloc<act_t>((size_t)B * src.in_H * src.in_W * src.in_Cp));
+    for (int r = 0; r < Rin; ++r) xin2_.push_back(alloc<act_t>((size_t)B * src.in_H * src.in_W * src.in_Cp));
     bytes_slot += (size_t)B * src.in_H * src.in_W * src.in_Cp * sizeof(act_t);
   }
   if (is_first()) xstage_ = alloc<float>((size_t)B * net.in_C * net.in_H * net.in_W);
@@ -253,15 +254,15 @@ void Stage::set_n_p(int64_t n_p) {
   PST_CUDA(cudaMemcpy(d_np_, &n_p, sizeof(int64_t), cudaMemcpyHostToDevice));
 }
 
-act_t* Stage::in_tensor(int l, int slot) const {
-  return l == l0 ? xin_[slot] : out_tensor(l - 1, slot);
+act_t* Stage::in_tensor(int l, int64_t mb) const {
+  return l == l0 ? xin_[mb % Rin] : out_tensor(l - 1, (int)(mb % R));
 }
 act_t* Stage::out_tensor(int l, int slot) const {
   const LayerBufs& b = L_[l - l0];
   if (!b.p.empty()) return b.p[slot];
   return b.z.empty() ? nullptr : b.z[slot];
 }
-act_t* Stage::output_slot(int slot) const { return out_tensor(l1 - 1, slot); }
+act_t* Stage::output_slot(int64_t mb) const { return out_tensor(l1 - 1, (int)(mb % R)); }
 act_t* Stage::dgrad_out() const { return L_[0].gin; }
 size_t Stage::input_bytes() const {
   const LayerInfo& f0 = net_.layers[l0];
@@ -290,18 +291,19 @@ size_t Stage::stage_x_bytes() const {
 }
 
 // ------------------------------------------------------------------ forward
-void Stage::enqueue_forward(int slot, cudaStream_t st) {
+void Stage::enqueue_forward(int64_t mb, cudaStream_t st) {
   const int B = batch_;
+  const int slot = (int)(mb % R);
   if (fwd_arena_n_) PST_CUDA(cudaMemsetAsync(fwd_arena_, 0, fwd_arena_n_ * sizeof(double), st));
   if (is_first())
-    input_to_act(xstage_, xin_[slot], B, net_.in_C, net_.in_H, net_.in_W, net_.in_Cp, st);
+    input_to_act(xstage_, xin_[mb % Rin], B, net_.in_C, net_.in_H, net_.in_W, net_.in_Cp, st);
   int bn_local = 0;
   for (int l = l0; l < l1; ++l) {
     const LayerInfo& li = net_.layers[l];
     LayerBufs& b = L_[l - l0];
     const bool last_net = (l == (int)net_.layers.size() - 1);
     ConvSpec c{};
-    c.in = in_tensor(l, slot);
+    c.in = in_tensor(l, mb);
     c.N = B;
     c.H = li.in_H;
     c.W = li.in_W;
@@ -341,7 +343,7 @@ void Stage::enqueue_forward(int slot, cudaStream_t st) {
       a.relu = li.spec.relu;
       if (li.spec.residual) {
         const LayerInfo& src = net_.layers[li.block_src];
-        a.res = li.block_src < l0 ? xin2_[slot] : in_tensor(li.block_src, slot);   // mid-block: received
+        a.res = li.block_src < l0 ? xin2_[mb % Rin] : in_tensor(li.block_src, mb);   // mid-block: received
         a.res_mode = li.res_mode;
         a.res_H = src.in_H; a.res_W = src.in_W; a.res_C = src.in_Cp; a.res_Creal = src.in_C;
         a.res_pad = li.res_pad;
@@ -364,8 +366,9 @@ void Stage::enqueue_forward(int slot, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ backward + update
-void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
+void Stage::enqueue_backward(int64_t mb, int dpar, cudaStream_t st) {
   const int B = batch_;
+  const int slot = (int)(mb % R);
   static const bool fuse_on = [] { const char* e = std::getenv("PST_FUSE_PRE"); return e == nullptr || e[0] != '0'; }();
   std::vector<char> pre_done(l1 - l0, 0);   // bwd_pre(l) already done by dgrad(l+1)'s epilogue
   PST_CUDA(cudaMemsetAsync(bwd_arena_, 0, bwd_arena_n_ * sizeof(double), st));
@@ -406,7 +409,7 @@ void Stage::enqueue_backward(int slot, int dpar, cudaStream_t st) {
     }
     // weight gradient from the saved input of this mini-batch
     WgradSpec wg{};
-    wg.x = in_tensor(l, slot);
+    wg.x = in_tensor(l, mb);
     wg.N = B;
     wg.H = li.in_H;
     wg.W = li.in_W;

@@ -36,14 +36,15 @@ class Stage {
   Stage(const Stage&) = delete;
   Stage& operator=(const Stage&) = delete;
 
-  // Enqueue work (capturable): forward of the mini-batch whose saved state lives in `slot`.
-  void enqueue_forward(int slot, cudaStream_t st);
-  // Backward + SGD update of the mini-batch in `slot`, reading the output gradient
-  // from dbuf[dpar] (non-last stages) or the stored dz (last stage).
-  void enqueue_backward(int slot, int dpar, cudaStream_t st);
+  // Enqueue work (capturable): forward of mini-batch mb (its saved state goes to ring slot mb % R,
+  // its input is read from input-ring slot mb % Rin).
+  void enqueue_forward(int64_t mb, cudaStream_t st);
+  // Backward + SGD update of mini-batch mb, reading the output gradient from dbuf[dpar] (non-last
+  // stages) or the stored dz (last stage).
+  void enqueue_backward(int64_t mb, int dpar, cudaStream_t st);
 
-  act_t* input_slot(int slot) const { return xin_[slot]; }
-  act_t* output_slot(int slot) const;            // stage output tensor (non-last stages)
+  act_t* input_slot(int64_t mb) const { return xin_[mb % Rin]; }
+  act_t* output_slot(int64_t mb) const;          // stage output tensor (non-last stages)
   act_t* dgrad_out() const;                      // gradient w.r.t. the stage input
   act_t* dbuf(int par) const { return dbuf_[par]; }
   size_t input_bytes() const;
@@ -54,11 +55,11 @@ class Stage {
   // input and sends its residual layer's pre-activation gradient back.
   bool ends_mid() const { return end_block_ >= 0; }
   bool starts_mid() const { return start_res_ >= 0; }
-  act_t* block_out(int slot) const { return in_tensor(end_block_, slot); }   // ends_mid: sent forward
+  act_t* block_out(int64_t mb) const { return in_tensor(end_block_, mb); }  // ends_mid: sent forward
   size_t block_out_bytes() const;
   act_t* dbuf2(int par) const { return dbuf2_[par]; }                         // ends_mid: received
   size_t dbuf2_bytes() const;
-  act_t* input2_slot(int slot) const { return xin2_[slot]; }                 // starts_mid: received
+  act_t* input2_slot(int64_t mb) const { return xin2_[mb % Rin]; }          // starts_mid: received
   size_t input2_bytes() const;
   act_t* sgrad_out() const { return L_[start_res_ - l0].gpre; }               // starts_mid: sent back
   size_t sgrad_bytes() const;
@@ -73,7 +74,10 @@ class Stage {
   int64_t read_version() const;
   void read_losses(int64_t first_mb, int64_t n, float* out) const;
 
-  const int s, K, l0, l1, dev, R, batch_;
+  const int s, K, l0, l1, dev;
+  const int R;     // saved-state ring slots (ring_saved)
+  const int Rin;   // input ring slots (ring_input)
+  const int batch_;
   int64_t p_base = 0, n_params = 0;
   size_t bytes_total = 0;   // device bytes this stage allocated
   size_t bytes_slot = 0;    // saved forward state of ONE mini-batch (input + per-layer y/z/pool/argmax/stats)
@@ -89,8 +93,8 @@ class Stage {
   const NetInfo& net_;
   std::vector<void*> allocs_;
   template <typename T> T* alloc(size_t n, bool zero = true);
-  act_t* in_tensor(int l, int slot) const;
-  act_t* out_tensor(int l, int slot) const;
+  act_t* in_tensor(int l, int64_t mb) const;     // input of layer l for mini-batch mb
+  act_t* out_tensor(int l, int slot) const;      // saved output of layer l in ring slot `slot`
 
   std::vector<LayerBufs> L_;
   std::vector<act_t*> xin_;
