@@ -9,7 +9,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # PST_LIB=bf16 / f16 selects another precision build (libpst_bf16.so / libpst_f16.so)
-_LIB_PATH = os.path.join(_HERE, {"bf16": "libpst_bf16.so", "f16": "libpst_f16.so"}.get(
+_LIB_PATH = os.path.join(_HERE, {"bf16": "libpst_bf16.so", "f16": "libpst_f16.so", "exp": "libpst_exp.so"}.get(
     os.environ.get("PST_LIB", ""), "libpst.so"))
 if os.environ.get("PST_LIB_PATH"):   # experiment builds (tools/); still the same C ABI
     _LIB_PATH = os.environ["PST_LIB_PATH"]

@@ -13,7 +13,8 @@ BUILD = os.path.join(ROOT, "build", "pst")
 LIB = os.path.join(HERE, "libpst.so")
 VARIANTS = {"": ("libpst.so", ()),                         # float32 storage, 3xTF32 tensor-core products
             "bf16": ("libpst_bf16.so", ("-DPST_PREC_BF16",)),  # fast variant (see DESIGN.md Precision)
-            "f16": ("libpst_f16.so", ("-DPST_ACT_FP16",))}     # diagnostics only
+            "f16": ("libpst_f16.so", ("-DPST_ACT_FP16",)),     # diagnostics only
+            "exp": ("libpst_exp.so", ("-DPST_EXPERIMENTS",))}  # default precision + experiment switches (tools/)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",

@@ -49,8 +49,18 @@ CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void* gaddr, const
   return m;
 }
 
+int pst_knob(const char* name, int dflt) {
+#ifdef PST_EXPERIMENTS
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
+}
+
 int wgrad_sms(int device) {
-  static const int over = [] { const char* e = std::getenv("PST_WG_SMS"); return e ? std::atoi(e) : 0; }();
+  static const int over = pst_knob("PST_WG_SMS", 0);
   const int n = num_sms(device);
   return over > 0 ? std::min(over, n) : n;
 }
@@ -119,10 +129,7 @@ void read(int cls, double* ms, int64_t* n, double* bytes, double* flops) {
 namespace pst {
 thread_local bool pdl_suppressed = false;
 bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PST_PDL");
-    return e == nullptr || e[0] != '0';
-  }();
+  static const bool on = pst_knob("PST_PDL", 1) != 0;
   return on;
 }
 }  // namespace pst

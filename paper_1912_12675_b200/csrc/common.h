@@ -121,6 +121,10 @@ int num_sms(int device);
 // wgrad runs on a forked stream beside the dgrad, so it can be given part of the GPU.
 int wgrad_sms(int device);
 
+// Experiment switches (environment variables) exist only in builds with -DPST_EXPERIMENTS
+// (tools/, A/B runs); the production library always takes the default.
+int pst_knob(const char* name, int dflt);
+
 // Launch accounting and optional per-kernel CUDA-event timing (bench.py's roofline).
 // ---------------------------------------------------------------- programmatic dependent launch
 // Every kernel of the step is launched with the PDL attribute: its CTAs may become resident and

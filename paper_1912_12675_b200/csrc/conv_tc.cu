@@ -1038,7 +1038,7 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
   bool halo = false;
   int nch_h = nch;
   // HALO by default where it applies (PST_NOHALO=1: per-tap loads everywhere, for comparison)
-  static const bool halo_on = std::getenv("PST_NOHALO") == nullptr;
+  static const bool halo_on = pst_knob("PST_NOHALO", 0) == 0;
   const int o1 = c.off, o2 = c.off + c.sgn * (c.k - 1);
   const int lo = std::min(o1, o2), hi = std::max(o1, o2);
   const int Wv = c.Wo + (hi - lo);   // virtual-grid row pitch = band row = output row + halo columns

@@ -26,6 +26,14 @@
 
 namespace pst {
 
+// Experiment switches inside the kernels (PST_TS_KNOB) and timeline probes exist only in
+// -DPST_EXPERIMENTS builds; in the production library they are compile-time zero.
+#ifdef PST_EXPERIMENTS
+#define KNOB(x) (a.knob & (x))
+#else
+#define KNOB(x) 0
+#endif
+
 #if PST_SPLIT
 namespace {
 
@@ -71,10 +79,14 @@ __device__ __forceinline__ unsigned long long ts_gtime() {
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));   // SM cycles (globaltimer reads are slow)
   return t;
 }
+#ifdef PST_EXPERIMENTS
 #define TSL(ev, i)                                                   \
   do {                                                               \
     if (a.dbg != nullptr && blockIdx.x == 0) { const int i_ = (i); if (i_ < 256) a.dbg[(ev) * 256 + i_] = ts_gtime(); } \
   } while (0)
+#else
+#define TSL(ev, i) do { } while (0)
+#endif
 
 __device__ __forceinline__ float ld_planar_f(const act_t* base, int64_t npix, int64_t pix, int c) {
   return act2f(base[((int64_t)(c / kEPC) * npix + pix) * kEPC + c % kEPC]);
@@ -152,7 +164,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   pdl_trigger();
   const uint32_t a_col0 = a.n_acc * a.accw;          // accumulators: columns [0, n_acc accw)
 
-  if (a.knob & 16) {
+  if (KNOB(16)) {
     // experiment: prologue and teardown only
   } else if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -180,7 +192,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         ptx::mbar_wait(&bempty[bs], bph ^ 1);
         if (lane == 0) TSL(0, dbg_i[0]++);
         if (ptx::elect_one()) {
-          if (a.knob & 32) { ptx::mbar_arrive(&full[bs]); } else {
+          if (KNOB(32)) { ptx::mbar_arrive(&full[bs]); } else {
           ptx::mbar_expect_tx(&full[bs], a.band_tx);
           ptx::tma_load_4d(bands + bs * a.band_bytes, &tmA, &full[bs], a.lo * kEPC, y0 * a.S + a.lo, n0,
                            kcc * (KC / kEPC));
@@ -206,15 +218,15 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     const int ngrp = a.taps / TPS;
     for (int m = m0; m < a.n_mtiles; m += mstep) {
       ptx::mbar_wait(&tempty[acc], aph ^ 1);
-      if (!(a.knob & 256)) ptx::tc_fence_after();
+      if (!KNOB(256)) ptx::tc_fence_after();
       const uint32_t d = tmem + acc * a.accw;
       for (int kcc = 0; kcc < a.n_kc; ++kcc) {
         for (int gi = 0; gi < ngrp; ++gi) {
           ptx::mbar_wait(&afull[slot], sph);
-          if (!(a.knob & 256)) ptx::tc_fence_after();
+          if (!KNOB(256)) ptx::tc_fence_after();
           if (lane == 0) TSL(4, dbg_i[4]++);
           if (ptx::elect_one()) {
-            if (!(a.knob & 2) && a.stack) {
+            if (!KNOB(2) && a.stack) {
 #pragma unroll
             for (int i = 0; i < TPS; ++i) {
               const int t = gi * TPS + i;
@@ -227,7 +239,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
                 ptx::umma_tf32_ts(d, ahi + KC + kk * 8, bd, idesc, 1u);                    // lo*hi
               }
             }
-            } else if (!(a.knob & 2)) {
+            } else if (!KNOB(2)) {
             // one slot = tps taps x (KC hi + KC lo columns): 3 x KC/8 x tps MMAs per handshake
             // compile-time trip counts: the elected lane's block is straight-line code (a runtime
             // loop here costs an R2UR round trip per tcgen05.mma, ~4x the small-N MMA time)
@@ -288,10 +300,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           if (++turn == kTsSets) turn = 0;
           if (!mine) continue;                               // another set's group
           ptx::mbar_wait(&aempty[my_slot], my_ph ^ 1);
-          if (!(a.knob & 256)) ptx::tc_fence_after();
+          if (!KNOB(256)) ptx::tc_fence_after();
           if (threadIdx.x == 192) TSL(1, dbg_i[1]++);
 #pragma unroll 1
-          for (int i = 0; i < TPS && !(a.knob & 1); ++i) {
+          for (int i = 0; i < TPS && !KNOB(1); ++i) {
             const int t = gi * TPS + i;
             const uint8_t* src = band + (uint32_t)(pixoff + tsh[t]) * 16;
             float hi[KC], lo[KC];
@@ -309,10 +321,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
               ptx::tmem_st16(ta + KC + h * 16, lo + 16 * h);
             }
           }
-          if ((a.knob & 1024) && threadIdx.x == 192) TSL(5, dbg_i[5]++);   // timeline: stores issued
-          if (!(a.knob & 512)) ptx::tmem_st_wait();
-          if ((a.knob & 1024) && threadIdx.x == 192) TSL(6, dbg_i[6]++);   // timeline: stores complete
-          if (!(a.knob & 256)) ptx::tc_fence_before();
+          if (KNOB(1024) && threadIdx.x == 192) TSL(5, dbg_i[5]++);   // timeline: stores issued
+          if (!KNOB(512)) ptx::tmem_st_wait();
+          if (KNOB(1024) && threadIdx.x == 192) TSL(6, dbg_i[6]++);   // timeline: stores complete
+          if (!KNOB(256)) ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&afull[my_slot]);
           if (threadIdx.x == 192) TSL(3, dbg_i[3]++);
@@ -375,11 +387,11 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         }
         if (g == 0) {
           ptx::mbar_wait(&tfull[acc], aph);
-          if (!(a.knob & 256)) ptx::tc_fence_after();
-          if (threadIdx.x == 64 && !(a.knob & 1024)) TSL(5, dbg_i[5]++);
+          if (!KNOB(256)) ptx::tc_fence_after();
+          if (threadIdx.x == 64 && !KNOB(1024)) TSL(5, dbg_i[5]++);
         }
         float u[16];
-        if (a.knob & 64) {
+        if (KNOB(64)) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) u[i] = 0.f;
         } else {
@@ -392,7 +404,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           }
         }
         if (g == ng - 1) {
-          if (!(a.knob & 256)) ptx::tc_fence_before();
+          if (!KNOB(256)) ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
           if (++acc == a.n_acc) { acc = 0; aph ^= 1; }
@@ -443,14 +455,14 @@ __global__ void __launch_bounds__(kTsThreads, 1)
             u[i] = (c < a.Cout) ? o : 0.f;
           }
         }
-        if (valid && !(a.knob & 8)) {
+        if (valid && !KNOB(8)) {
           float* o = reinterpret_cast<float*>(a.out);   // act_t == float in this build
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj)
             *reinterpret_cast<float4*>(o + ((int64_t)(c0 / 4 + jj) * npix + pix) * 4) =
                 make_float4(u[4 * jj], u[4 * jj + 1], u[4 * jj + 2], u[4 * jj + 3]);
         }
-        if (EPI == EPI_BN_STATS && !(a.knob & 4)) {
+        if (EPI == EPI_BN_STATS && !KNOB(4)) {
           float s1[16], s2[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) { s1[i] = u[i]; s2[i] = u[i] * u[i]; }
@@ -477,7 +489,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
           warp_chan_sums(s1, s2, lane, wacc + q * 2 * a.BN + 2 * (g * 16 + (lane >> 1)));
         }
       }
-      if (threadIdx.x == 64 && !(a.knob & 1024)) TSL(6, dbg_i[6]++);
+      if (threadIdx.x == 64 && !KNOB(1024)) TSL(6, dbg_i[6]++);
     }
     if (sums) {
       double* dst = EPI == EPI_BN_STATS ? a.stats : a.bsums;
@@ -501,7 +513,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
 
 // Plans the TS kernel for this convolution; false if the shape does not fit its tiling.
 static bool ts_plan(const ConvSpec& c, TsArgs& a, int& kc) {
-  if (std::getenv("PST_NOTS") != nullptr) return false;
+  if (pst_knob("PST_NOTS", 0)) return false;
   if (c.k > 7 || (c.S != 1 && c.S != 2) || c.Coutp > 256) return false;
   if (c.Wo > 128 || 128 % c.Wo != 0) return false;
   const int per_img = c.Ho * c.Wo;
@@ -527,16 +539,16 @@ static bool ts_plan(const ConvSpec& c, TsArgs& a, int& kc) {
   a.band_bytes = (uint32_t)round_up((int)a.band_tx, 1024);
   // N tile: resident hi+lo weights of all taps <= wmax KB (PST_TS_WMAX: planning experiments;
   // 150 lets the 64-channel convs take BN = 32: half the N tiles, each MMA twice as wide)
-  static const int wmax = [] { const char* e = std::getenv("PST_TS_WMAX"); return e ? std::atoi(e) : 150; }();
-  static const int force_tps = [] { const char* e = std::getenv("PST_TS_TPS"); return e ? std::atoi(e) : 0; }();
-  static const int force_nacc = [] { const char* e = std::getenv("PST_TS_NACC"); return e ? std::atoi(e) : 0; }();
+  static const int wmax = pst_knob("PST_TS_WMAX", 150);
+  static const int force_tps = pst_knob("PST_TS_TPS", 0);
+  static const int force_nacc = pst_knob("PST_TS_NACC", 0);
   a.BN = 0;
   for (int bn = std::min(c.Coutp, 128); bn >= 16; bn -= 16)
     if (c.Coutp % bn == 0 && 2ll * a.taps * c.Cinp * bn * 4 <= (int64_t)wmax * 1024) { a.BN = bn; break; }
   if (a.BN == 0) return false;
   a.n_ntiles = c.Coutp / a.BN;
   a.w_bytes = (uint32_t)a.taps * c.Cinp * a.BN * 4;
-  static const bool stack_on = [] { const char* e = std::getenv("PST_TS_STACK"); return e == nullptr || e[0] != '0'; }();
+  static const bool stack_on = pst_knob("PST_TS_STACK", 1) != 0;
   a.stack = (stack_on && a.BN * kEPC <= 256) ? 1 : 0;
   a.accw = a.stack ? 2 * a.BN : a.BN;
   const int fixed = 2 * (int)a.w_bytes + 4 * 32 * 17 * 4 + 2048 + (2 * kMaxBand + 2 * kMaxSlots + 2 * kMaxAcc + 1) * 8 + 16 + 256;
@@ -579,7 +591,7 @@ bool conv_ts(const ConvSpec& c, cudaStream_t st) {
   a.bz = c.bz; a.by = c.by; a.bsaved = c.bsaved; a.bsums = c.bsums;
   a.bfuse = c.bfuse; a.brelu = c.brelu; a.bbn = c.bbn;
   a.bscale = c.bscale == 0.f ? 1.f : c.bscale;
-  { static const char* kn = std::getenv("PST_TS_KNOB"); a.knob = kn ? std::atoi(kn) : 0; }
+  { static const int kn = pst_knob("PST_TS_KNOB", 0); a.knob = kn; }
   // band box: (Wb*EPC, Hb, nb images, KC/EPC planes) of the planar input, zero outside
   uint64_t dims[4] = {(uint64_t)c.W * kEPC, (uint64_t)c.H, (uint64_t)c.N, (uint64_t)c.Cinp / kEPC};
   uint64_t str[3] = {(uint64_t)c.W * 16, (uint64_t)c.H * c.W * 16, (uint64_t)c.N * c.H * c.W * 16};

@@ -44,6 +44,7 @@ struct WtArgs {
   float* part;
   unsigned long long* dbg;   // optional timeline (CTA 0, clock64), PST_DBG_TL
 };
+#ifdef PST_EXPERIMENTS
 #define WTL(ev, i)                                                                        \
   do {                                                                                   \
     if (a.dbg != nullptr && blockIdx.x == 0) {                                           \
@@ -53,6 +54,9 @@ struct WtArgs {
       if (i_ < 256) a.dbg[(ev) * 256 + i_] = t_;                                         \
     }                                                                                    \
   } while (0)
+#else
+#define WTL(ev, i) do { } while (0)
+#endif
 
 template <int G, int P16, int SETS>
 __global__ void __launch_bounds__(wt_threads(SETS), 1)
@@ -311,7 +315,7 @@ int tile_n16(int C, int cap) {
 
 bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm,
                    void* out) {
-  if (std::getenv("PST_NOTS") != nullptr) return false;
+  if (pst_knob("PST_NOTS", 0)) return false;
   WtArgs a{};
   a.N = N; a.H = H; a.W = W; a.Cinp = Cinp; a.Ho = Ho; a.Wo = Wo; a.Coutp = Coutp;
   a.k = k; a.S = S; a.pad = pad;
@@ -320,7 +324,7 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   a.BNw = tile_n16(Coutp, 128);
   a.n_ntiles = Coutp / a.BNw;
   // pixels per unit (PST_WT_PTARGET experiments: 64 halves the per-unit hand-offs, needs G = 1)
-  static const int ptarget = [] { const char* e = std::getenv("PST_WT_PTARGET"); return e ? std::atoi(e) : 32; }();
+  static const int ptarget = pst_knob("PST_WT_PTARGET", 32);
   if (Ho * Wo >= ptarget) { a.nb = 1; a.bh = std::max(1, std::min(Ho, ptarget / Wo)); }
   else { a.nb = std::max(1, std::min(N, ptarget / (Ho * Wo))); a.bh = Ho; }
   a.P = a.nb * a.bh * Wo;
@@ -352,7 +356,7 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   // a third converter set (three units in flight) where the slots allow it without shrinking G:
   // a set reuses a slot / band stage only after the unit SETS earlier waited on it (mbarrier
   // parity aliasing), so St >= SETS and SB >= SETS
-  static const int max_sets = [] { const char* e = std::getenv("PST_WT_SETS"); return e ? std::atoi(e) : 3; }();
+  static const int max_sets = pst_knob("PST_WT_SETS", 3);
   // (measured: g1 wgrad 24.2 -> 21.3 us with 3 sets; the 576-row g3 gets slower, so only the
   // small-row layers take it)
   a.sets = (max_sets >= 3 && a.St >= 3 && a.SB >= 3 && a.rows <= 256) ? 3 : 2;
@@ -362,9 +366,9 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   const int base = a.n_mgroups * a.n_ntiles;
   a.ksplit = std::max(1, std::min(std::max(1, a.n_units / 2), num_sm / base));
   // cap on the split (PST_WT_KSPLIT_MAX experiments): fewer fp32 partials to write and reduce
-  static const int ks_max = [] { const char* e = std::getenv("PST_WT_KSPLIT_MAX"); return e ? std::atoi(e) : 0; }();
+  static const int ks_max = pst_knob("PST_WT_KSPLIT_MAX", 0);
   if (ks_max > 0) a.ksplit = std::min(a.ksplit, ks_max);
-  static const int ks_big = [] { const char* e = std::getenv("PST_WT_KSPLIT_MAX_BIG"); return e ? std::atoi(e) : 0; }();
+  static const int ks_big = pst_knob("PST_WT_KSPLIT_MAX_BIG", 0);
   if (ks_big > 0 && a.rows > 256) a.ksplit = std::min(a.ksplit, ks_big);   // the many-row (64-channel) layers only
   if (out) *reinterpret_cast<WtArgs*>(out) = a;
   return true;

@@ -69,7 +69,7 @@ int pst_op_conv2d_fwd(const float* x, const float* w, float* y, int N, int Cin, 
     c.Ho = g.Ho; c.Wo = g.Wo; c.Coutp = g.Coutp; c.Cout = Cout;
     c.k = k; c.S = stride; c.off = -pad; c.sgn = 1;
     c.wshadow = sf; c.epi = EPI_BIAS_F32; c.out = yo;
-    const bool tl = std::getenv("PST_DBG_TL") != nullptr;
+    const bool tl = pst_knob("PST_DBG_TL", 0) != 0;
     if (tl) c.dbg = s.get<unsigned long long>(8 * 256);
     conv_tc(c, 0);
     if (tl) {  // debug: print CTA 0's timeline (us since kernel start)
@@ -134,7 +134,7 @@ int pst_op_conv2d_wgrad(const float* x, const float* gy, float* gw, int N, int C
     wg.x = xa; wg.N = N; wg.H = H; wg.W = W; wg.Cinp = g.Cinp;
     wg.dy = ga; wg.Ho = g.Ho; wg.Wo = g.Wo; wg.Coutp = g.Coutp;
     wg.k = k; wg.S = stride; wg.pad = pad; wg.part = part; wg.ksplit = p.ksplit;
-    const bool tl = std::getenv("PST_DBG_TL") != nullptr;
+    const bool tl = pst_knob("PST_DBG_TL", 0) != 0;
     if (tl) wg.dbg = s.get<unsigned long long>(8 * 256);
     conv_wgrad_tc(wg, 0);
     if (tl) {

@@ -12,14 +12,19 @@ namespace pst {
 // Timing experiments only (PST_SKIP=fwd,bnapply,bwdpre,bnbwd,wgrad,dgrad,sgd): leave a kernel class
 // out of the step to measure its in-graph cost.  Results are wrong when set.
 static bool side_wgrad() {
-  static const bool on = [] { const char* e = std::getenv("PST_WSTREAM"); return e == nullptr || e[0] != '0'; }();
+  static const bool on = pst_knob("PST_WSTREAM", 1) != 0;
   // the per-kernel event profile (pst_profile) times launches one at a time: a wgrad running
   // beside the dgrad would be charged the time it waits for SMs
   return on && !prof::enabled;
 }
 static bool skip(const char* cls) {
+#ifdef PST_EXPERIMENTS
   static const char* env = std::getenv("PST_SKIP");
   return env != nullptr && std::strstr(env, cls) != nullptr;
+#else
+  (void)cls;
+  return false;
+#endif
 }
 
 // Dropout threshold and scale from the float32 probability (pst.h pst_layer.dropout).
@@ -369,7 +374,7 @@ void Stage::enqueue_forward(int64_t mb, cudaStream_t st) {
 void Stage::enqueue_backward(int64_t mb, int dpar, cudaStream_t st) {
   const int B = batch_;
   const int slot = (int)(mb % R);
-  static const bool fuse_on = [] { const char* e = std::getenv("PST_FUSE_PRE"); return e == nullptr || e[0] != '0'; }();
+  static const bool fuse_on = pst_knob("PST_FUSE_PRE", 1) != 0;
   std::vector<char> pre_done(l1 - l0, 0);   // bwd_pre(l) already done by dgrad(l+1)'s epilogue
   PST_CUDA(cudaMemsetAsync(bwd_arena_, 0, bwd_arena_n_ * sizeof(double), st));
   for (int l = l1 - 1; l >= l0; --l) {
@@ -424,7 +429,7 @@ void Stage::enqueue_backward(int64_t mb, int dpar, cudaStream_t st) {
       if (side_wgrad()) {
         PST_CUDA(cudaEventRecord(ev_fork, st));
         PST_CUDA(cudaStreamWaitEvent(wstream, ev_fork, 0));
-        static const bool wg_pdl = [] { const char* e = std::getenv("PST_WG_PDL"); return e == nullptr || e[0] != '0'; }();
+        static const bool wg_pdl = pst_knob("PST_WG_PDL", 1) != 0;
         pdl_suppressed = !wg_pdl;
         conv_wgrad_tc(wg, wstream);
         pdl_suppressed = false;
@@ -476,7 +481,7 @@ void Stage::enqueue_backward(int64_t mb, int dpar, cudaStream_t st) {
         c.res_mode = e.res_mode;
         c.res_H = e.Ho; c.res_W = e.Wo; c.res_C = e.Coutp; c.res_pad = e.res_pad;
       }
-      static const int dg_ctas = [] { const char* e = std::getenv("PST_DG_CTAS"); return e ? std::atoi(e) : 0; }();
+      static const int dg_ctas = pst_knob("PST_DG_CTAS", 0);
       c.max_ctas = side_wgrad() ? dg_ctas : 0;
       if (!skip("dgrad")) conv_tc(c, st);
     }
