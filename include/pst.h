@@ -99,12 +99,31 @@ typedef struct {
 
 /* Pipeline Placement Vector: ppv[i] is the 1-indexed weighted layer
  * after which register pair i sits; stage s holds layers ppv[s-1]+1..ppv[s]
- * (reading AMB-13).  Strictly increasing, in [1, n_layers-1], not inside a
- * residual block (mid-block registers return PST_E_UNSUPPORTED). */
+ * (reading AMB-13).  Strictly increasing, in [1, n_layers-1].  A point inside a
+ * residual block is a two-tensor register (reading AMB-14; at most
+ * one point per block, else PST_E_UNSUPPORTED).
+ *
+ * mapping (section 3, section 6.5):
+ *   PST_MAP_PER_GPU (0)  one accelerator per stage runs FS_i and BKS_{K_p-i+2}
+ *                        (the paper's 2-GPU implementation); `devices` has
+ *                        K entries.
+ *   PST_MAP_FS_BKS  (1)  the paper's 2K_p+1-accelerator mapping: the
+ *                        forward stage and the backward stage of every stage but
+ *                        the last run on separate accelerators; the last stage's FS
+ *                        and BKS share one (forward, then backward of the same
+ *                        mini-batch).  Each cycle the BKS forwards its new weights
+ *                        to its FS and the FS sends the saved activations
+ *                        to its BKS.  Same weight versions as mapping 0.
+ *                        `devices` has 2K-1 entries: FS of stages 0..K-1, then BKS
+ *                        of stages 0..K-2.  Local mode only; no hybrid switch
+ *                        (PST_E_UNSUPPORTED). */
+#define PST_MAP_PER_GPU 0
+#define PST_MAP_FS_BKS 1
 typedef struct {
   int32_t n_stages;          /* K >= 1 */
   const int32_t* ppv;        /* K-1 entries (may be NULL when K == 1) */
-  const int32_t* devices;    /* K CUDA device ordinals (NULL: all on device 0) */
+  const int32_t* devices;    /* CUDA device ordinals, see mapping (NULL: all on device 0) */
+  int32_t mapping;           /* PST_MAP_PER_GPU or PST_MAP_FS_BKS */
 } pst_partition;
 
 typedef struct {

@@ -227,6 +227,88 @@ def run_clocked(stages, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce, n_
     return Result(losses, W, mom, log, snaps if snapshot else None, stages=stages)
 
 
+def run_fs_bks(stages, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce):
+    """Oracle C: the paper's own accelerator mapping (Fig. 3/4; SURVEY f-4).
+
+    K = K_p + 1 stages; the forward stage FS_s and the backward stage BKS_s of stage s run on
+    separate accelerators, except the last stage, whose FS and BKS share one ("FS_{K+1} and BKS_1
+    ... are assigned to the same accelerator to reduce weight staleness by an execution cycle",
+    L67) -- 2K_p + 1 accelerators in total (L67, L77).  One execution cycle t (L61), all
+    accelerators in parallel, messages produced in cycle t visible in cycle t+1:
+      FS_s, s < K-1 : forward of mini-batch f = t - s with its copy of the weights; the activation
+                      goes to FS_{s+1}, the saved activations (L65) to BKS_s;
+      last stage    : forward of f = t - (K-1), the loss, then the backward and update of the SAME
+                      mini-batch with the same (current) weights; the error goes to BKS_{K-2};
+      BKS_s, s < K-1: backward + update of b = t - 2K + 2 + s with the current weights and the saved
+                      activations of b; the error goes to BKS_{s-1}; the new weights go to FS_s
+                      (weight forwarding), which uses them from cycle t+1.
+    FS_s therefore reads version f - 2(K-1-s) (clamped at 0): the degree of staleness
+    2(K_p - i + 1) of L75, the same versions Oracle A defines -- A == C bitwise is the pin."""
+    K = len(stages)
+    N = len(batches)
+    W = [params0[s] for s in range(K)]                # BKS (master) weights; last stage: the only copy
+    Wf = [params0[s] for s in range(K)]               # FS copies (forwarded weights)
+    mom = [_zeros_like(params0[s]) for s in range(K)]
+    v = [0] * K
+    saved = [dict() for _ in range(K)]                # BKS_s inbox of saved activations
+    inbox_f = [dict() for _ in range(K)]
+    inbox_b = [dict() for _ in range(K)]
+    losses = [None] * N
+    log = []
+    t = 0
+    last_t = N - 1 + 2 * K - 2 if N > 0 else -1       # stage 0's BKS handles mini-batch N-1 at N-1+2K-2
+    while t <= last_t:
+        out_f, out_b, out_saved, out_w = [], [], [], []
+        for s in range(K):
+            f = t - s
+            if s == K - 1:
+                if 0 <= f < N:
+                    a_in = batches[f][0] if s == 0 else inbox_f[s].pop(f)
+                    log.append((t, s, "F", f, v[s]))
+                    out, cache = stages[s].forward(W[s], a_in, mb=f)
+                    losses[f], g = loss_fn(out, batches[f][1])
+                    assert v[s] == f, (t, s, v[s], f)
+                    log.append((t, s, "B", f, v[s]))
+                    g, G = stages[s].backward(W[s], cache, g)
+                    W[s], mom[s] = _sgd_stage(W[s], mom[s], G, learning_rate(hp, s, f), hp)
+                    v[s] += 1
+                    if s > 0:
+                        out_b.append((s - 1, f, g))
+                continue
+            b = t - 2 * K + 2 + s
+            if 0 <= b < N:                             # BKS_s
+                assert v[s] == b, (t, s, v[s], b)
+                log.append((t, s, "B", b, v[s]))
+                g, G = stages[s].backward(W[s], saved[s].pop(b), inbox_b[s].pop(b))
+                W[s], mom[s] = _sgd_stage(W[s], mom[s], G, learning_rate(hp, s, b), hp)
+                v[s] += 1
+                out_w.append((s, W[s]))
+                if s > 0:
+                    out_b.append((s - 1, b, g))
+            if 0 <= f < N:                             # FS_s
+                a_in = batches[f][0] if s == 0 else inbox_f[s].pop(f)
+                log.append((t, s, "F", f, v_fs(s, t, K, N)))
+                out, cache = stages[s].forward(Wf[s], a_in, mb=f)
+                out_f.append((s + 1, f, out))
+                out_saved.append((s, f, cache))
+        for (s, f, a) in out_f:
+            inbox_f[s][f] = a
+        for (s, b, g) in out_b:
+            inbox_b[s][b] = g
+        for (s, f, c) in out_saved:
+            saved[s][f] = c
+        for (s, w) in out_w:
+            Wf[s] = w
+        t += 1
+    assert all(not d for d in saved) and all(not d for d in inbox_b)
+    return Result(losses, W, mom, log, stages=stages)
+
+
+def v_fs(s, t, K, N):
+    """Version held by FS_s during cycle t of Oracle C: the BKS_s updates of cycles < t."""
+    return max(0, min(N, t - 2 * K + 2 + s))
+
+
 def run_sgd(stage, params0, batches, hp: HParams, loss_fn=Lx.softmax_ce):
     """Textbook non-pipelined mini-batch SGD over the whole network as one stage
     (§2): forward, loss, backward, update -- one mb at a time."""

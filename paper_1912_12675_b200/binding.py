@@ -39,7 +39,10 @@ class _Net(C.Structure):
 
 
 class _Partition(C.Structure):
-    _fields_ = [("n_stages", C.c_int32), ("ppv", C.POINTER(C.c_int32)), ("devices", C.POINTER(C.c_int32))]
+    _fields_ = [("n_stages", C.c_int32), ("ppv", C.POINTER(C.c_int32)), ("devices", C.POINTER(C.c_int32)),
+                ("mapping", C.c_int32)]
+
+MAP_PER_GPU, MAP_FS_BKS = 0, 1
 
 
 class _HParams(C.Structure):
@@ -146,13 +149,13 @@ def net_struct(net, params: Optional[np.ndarray] = None):
     return n, keep
 
 
-def _partition(ppv, devices=None):
+def _partition(ppv, devices=None, mapping=0):
     K = len(ppv) + 1
     pp = (C.c_int32 * max(1, K - 1))(*ppv)
-    part = _Partition(K, C.cast(pp, C.POINTER(C.c_int32)), None)
+    part = _Partition(K, C.cast(pp, C.POINTER(C.c_int32)), None, mapping)
     keep = [pp]
     if devices is not None:
-        dv = (C.c_int32 * K)(*devices)
+        dv = (C.c_int32 * len(devices))(*devices)
         part.devices = C.cast(dv, C.POINTER(C.c_int32))
         keep.append(dv)
     return part, keep
@@ -196,13 +199,13 @@ class Pipeline:
                  devices: Optional[Sequence[int]] = None, rank: Optional[int] = None,
                  nccl_id: Optional[bytes] = None, solver: str = "torch", nesterov: bool = False,
                  lr_policy: str = "multistep", inv_gamma: float = 0.0, inv_power: float = 0.0,
-                 dropout_seed: int = 0):
+                 dropout_seed: int = 0, mapping: int = 0):
         L = lib()
         self.net = net
         self.K = len(ppv) + 1
         self.batch = batch
         n, self._keep_net = net_struct(net, params)
-        part, self._keep_part = _partition(list(ppv), devices)
+        part, self._keep_part = _partition(list(ppv), devices, mapping)
         lrs = (C.c_float * self.K)(*lr_pipelined)
         ms = (C.c_int64 * max(1, len(milestones)))(*milestones)
         hp = _HParams(batch, momentum, weight_decay, C.cast(lrs, C.POINTER(C.c_float)), lr_nonpipelined,

@@ -57,6 +57,10 @@ struct pst_ctx {
   int rank = 0;
   ncclComm_t comm = nullptr;
   std::vector<std::unique_ptr<Stage>> stages;   // local: K stages; dist: 1 (stage == rank)
+  // PST_MAP_FS_BKS: stages[s] is FS_s (the last stage does both), bks[s] is BKS_s, s < K-1
+  int mapping = PST_MAP_PER_GPU;
+  std::vector<std::unique_ptr<Stage>> bks;
+  std::vector<cudaEvent_t> bdone, wev;          // per BKS: last step's work / new weights ready
   std::vector<int> devices;
   pst_hparams hp{};
   std::vector<float> lr_pipe;
@@ -74,6 +78,7 @@ struct pst_ctx {
   int mode = MODE_PIPE;
   bool use_graphs = true;
   std::vector<std::map<GraphKey, GraphEntry>> graphs;        // per owned stage
+  std::vector<std::map<GraphKey, GraphEntry>> graphs_b;      // per BKS object (PST_MAP_FS_BKS)
   std::vector<cudaEvent_t> done;                              // per owned stage: last step's work
   // host staging (pinned) for the batch
   float* pin_x[2] = {nullptr, nullptr};
@@ -234,14 +239,13 @@ static void enqueue_np(pst_ctx* c, int s, int64_t i, bool fwd, cudaStream_t st) 
 }
 
 template <typename F>
-static void run_program(pst_ctx* c, int s, const GraphKey& key, F&& enqueue) {
-  Stage* S = c->stage(s);
+static void run_program(pst_ctx* c, Stage* S, std::map<GraphKey, GraphEntry>& cache, const GraphKey& key,
+                        F&& enqueue) {
   PST_CUDA(cudaSetDevice(S->dev));
   if (!c->use_graphs || prof::enabled) {   // profiling runs eagerly: events bracket each kernel
     enqueue(S->stream);
     return;
   }
-  auto& cache = c->graphs[c->local_index(s)];
   auto it = cache.find(key);
   if (it == cache.end()) {
     cudaGraph_t g;
@@ -263,6 +267,11 @@ static void run_program(pst_ctx* c, int s, const GraphKey& key, F&& enqueue) {
   }
   PST_CUDA(cudaGraphLaunch(it->second.exec, S->stream));
   prof::launches += it->second.kernels;
+}
+
+template <typename F>
+static void run_program(pst_ctx* c, int s, const GraphKey& key, F&& enqueue) {
+  run_program(c, c->stage(s), c->graphs[c->local_index(s)], key, std::forward<F>(enqueue));
 }
 
 // In local mode stage s's step depends on its neighbours' previous step.
@@ -331,11 +340,105 @@ static void pipe_step(pst_ctx* c) {
   c->t += 1;
 }
 
+// One cycle of the paper's 2K_p+1-accelerator mapping (PST_MAP_FS_BKS; Oracle C in
+// oracle/pipeline.py run_fs_bks).  Cycle t: FS_s forwards f = t-s with the weights its BKS forwarded
+// at the end of cycle t-1 and hands the saved activations of f to BKS_s; the last stage forwards f
+// and then runs the backward + update of the same f; BKS_s (s < K-1) runs the backward + update of
+// b = t-2K+2+s and forwards its new weights to FS_s, which installs them after its own forward of
+// this cycle.  All messages of cycle t are consumed in cycle t+1 (events between the objects).
+static void fsbks_step(pst_ctx* c) {
+  const int K = c->K;
+  const int64_t rel = c->t - c->t0, P = ring_period(K);
+  auto valid = [&](int64_t mb) { return mb >= c->m0 && mb < c->n_fed ? mb : (int64_t)-1; };
+  auto m = [P](int64_t mb) { return mb >= 0 ? mb % P : -1; };
+  std::vector<int64_t> f(K), b(K);
+  for (int s = 0; s < K; ++s) {
+    f[s] = valid(c->m0 + rel - s);
+    b[s] = s == K - 1 ? f[s] : valid(c->m0 + rel - 2 * K + 2 + s);
+  }
+  if (f[K - 1] >= 0) c->n_loss = std::max(c->n_loss, f[K - 1] + 1);
+  // waits on the previous cycle (all before any launch)
+  for (int s = 0; s < K; ++s) {
+    Stage* F = c->stages[s].get();
+    if (s > 0) PST_CUDA(cudaStreamWaitEvent(F->stream, c->done[s - 1], 0));    // activation of f
+    if (s < K - 1) {
+      Stage* Bk = c->bks[s].get();
+      PST_CUDA(cudaStreamWaitEvent(Bk->stream, c->done[s], 0));                 // saved state of b
+      PST_CUDA(cudaStreamWaitEvent(Bk->stream, s + 1 < K - 1 ? c->bdone[s + 1] : c->done[K - 1], 0));   // error of b
+    }
+  }
+  // BKS_s: backward + update of b, error to BKS_{s-1}, new weights ready
+  for (int s = 0; s + 1 < K; ++s) {
+    if (b[s] < 0) continue;
+    Stage* Bk = c->bks[s].get();
+    GraphKey key;
+    key.k = {4, m(b[s])};
+    PST_CUDA(cudaSetDevice(Bk->dev));
+    const int64_t bb = b[s];
+    run_program(c, Bk, c->graphs_b[s], key, [&](cudaStream_t st) {
+      Bk->enqueue_backward(bb, (int)(bb & 1), st);
+      if (s > 0) {
+        Stage* D = c->bks[s - 1].get();
+        PST_CUDA(cudaMemcpyAsync(D->dbuf((int)(bb & 1)), Bk->dgrad_out(), D->output_bytes(), cudaMemcpyDefault, st));
+        if (Bk->starts_mid())
+          PST_CUDA(cudaMemcpyAsync(D->dbuf2((int)(bb & 1)), Bk->sgrad_out(), Bk->sgrad_bytes(), cudaMemcpyDefault, st));
+      }
+    });
+    PST_CUDA(cudaEventRecord(c->wev[s], Bk->stream));
+  }
+  // FS_s: forward of f (+ the last stage's backward of the same f), activation to FS_{s+1}, saved
+  // state to BKS_s; then the weights BKS_s produced in this cycle
+  for (int s = 0; s < K; ++s) {
+    Stage* F = c->stages[s].get();
+    PST_CUDA(cudaSetDevice(F->dev));
+    if (f[s] >= 0) {
+      GraphKey key;
+      key.k = {3, m(f[s])};
+      const int64_t ff = f[s];
+      run_program(c, F, c->graphs[s], key, [&](cudaStream_t st) {
+        F->enqueue_forward(ff, st);
+        if (s < K - 1) {
+          Stage* D = c->stages[s + 1].get();
+          PST_CUDA(cudaMemcpyAsync(D->input_slot(ff), F->output_slot(ff), F->output_bytes(), cudaMemcpyDefault, st));
+          if (F->ends_mid())
+            PST_CUDA(cudaMemcpyAsync(D->input2_slot(ff), F->block_out(ff), F->block_out_bytes(), cudaMemcpyDefault, st));
+          F->copy_saved_to(*c->bks[s], ff, st);
+        } else {
+          F->enqueue_backward(ff, 0, st);   // the last stage: FS_{K_p+1} and BKS_1 on one accelerator
+          if (s > 0) {
+            Stage* D = c->bks[s - 1].get();
+            PST_CUDA(cudaMemcpyAsync(D->dbuf((int)(ff & 1)), F->dgrad_out(), D->output_bytes(), cudaMemcpyDefault, st));
+            if (F->starts_mid())
+              PST_CUDA(cudaMemcpyAsync(D->dbuf2((int)(ff & 1)), F->sgrad_out(), F->sgrad_bytes(), cudaMemcpyDefault, st));
+          }
+        }
+      });
+    }
+    if (s < K - 1 && b[s] >= 0) {      // weight forwarding BKS_s -> FS_s (after this cycle's forward)
+      PST_CUDA(cudaStreamWaitEvent(F->stream, c->wev[s], 0));
+      F->copy_weights_from(*c->bks[s], F->stream);
+    }
+  }
+  for (int s = 0; s < K; ++s) {
+    PST_CUDA(cudaSetDevice(c->stages[s]->dev));
+    PST_CUDA(cudaEventRecord(c->done[s], c->stages[s]->stream));
+    if (s < K - 1) {
+      PST_CUDA(cudaSetDevice(c->bks[s]->dev));
+      PST_CUDA(cudaEventRecord(c->bdone[s], c->bks[s]->stream));
+    }
+  }
+  c->t += 1;
+}
+
 static void drain(pst_ctx* c) {
   if (c->mode != MODE_PIPE) return;
   // the last backward is stage 0's of mini-batch n_fed-1 at relative step n_fed-1-m0 + 2K-1
-  const int64_t last = c->t0 + (c->n_fed - 1 - c->m0) + 2 * c->K - 1;
-  while (c->n_fed > c->m0 && c->t <= last) pipe_step(c);
+  // (FS/BKS mapping: one cycle earlier, BKS_0 at n_fed-1-m0 + 2K-2)
+  const int64_t last = c->t0 + (c->n_fed - 1 - c->m0) + 2 * c->K - 1 - (c->mapping == PST_MAP_FS_BKS ? 1 : 0);
+  while (c->n_fed > c->m0 && c->t <= last) {
+    if (c->mapping == PST_MAP_FS_BKS) fsbks_step(c);
+    else pipe_step(c);
+  }
   c->t0 = c->t;
   c->m0 = c->n_fed;
 }
@@ -372,10 +475,11 @@ static void np_step(pst_ctx* c) {
 }
 
 static void sync_all(pst_ctx* c) {
-  for (auto& S : c->stages) {
-    PST_CUDA(cudaSetDevice(S->dev));
-    PST_CUDA(cudaStreamSynchronize(S->stream));
-  }
+  for (auto* v : {&c->stages, &c->bks})
+    for (auto& S : *v) {
+      PST_CUDA(cudaSetDevice(S->dev));
+      PST_CUDA(cudaStreamSynchronize(S->stream));
+    }
 }
 
 // ------------------------------------------------------------------ ABI
@@ -410,8 +514,13 @@ int pst_create(const pst_net* net, const pst_partition* part, const pst_hparams*
     int ndev = 0;
     PST_CUDA(cudaGetDeviceCount(&ndev));
     PST_CHECK_ARG(ndev >= 1, "no CUDA device");
-    c->devices.resize(c->K);
-    for (int s = 0; s < c->K; ++s) {
+    PST_CHECK_ARG(part->mapping == PST_MAP_PER_GPU || part->mapping == PST_MAP_FS_BKS, "mapping");
+    c->mapping = part->mapping;
+    if (c->mapping == PST_MAP_FS_BKS && dist)
+      throw Unsupported("the FS/BKS mapping runs in local mode only (one process drives all 2K-1 accelerators)");
+    const int ndevs = c->mapping == PST_MAP_FS_BKS ? 2 * c->K - 1 : c->K;
+    c->devices.resize(ndevs);
+    for (int s = 0; s < ndevs; ++s) {
       c->devices[s] = part->devices ? part->devices[s] : 0;
       PST_CHECK_ARG(c->devices[s] >= 0 && c->devices[s] < ndev, "device ordinal");
     }
@@ -433,9 +542,22 @@ int pst_create(const pst_net* net, const pst_partition* part, const pst_hparams*
       c->done.push_back(e);
     }
     c->graphs.resize(c->stages.size());
+    if (c->mapping == PST_MAP_FS_BKS) {   // BKS_s objects on their own accelerators
+      for (int s = 0; s + 1 < c->K; ++s) {
+        c->bks.emplace_back(new Stage(c->net, s, c->K, c->ranges[s].first, c->ranges[s].second, c->devices[c->K + s],
+                                      c->hp, net->init_params, c->batch));
+        cudaEvent_t e1, e2;
+        PST_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+        PST_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+        PST_CUDA(cudaEventRecord(e1, c->bks.back()->stream));
+        c->bdone.push_back(e1);
+        c->wev.push_back(e2);
+      }
+      c->graphs_b.resize(c->bks.size());
+    }
     if (!c->dist) {  // peer access between distinct stage devices (best effort)
-      for (int a = 0; a < c->K; ++a)
-        for (int b = 0; b < c->K; ++b) {
+      for (int a = 0; a < (int)c->devices.size(); ++a)
+        for (int b = 0; b < (int)c->devices.size(); ++b) {
           if (c->devices[a] == c->devices[b]) continue;
           int ok = 0;
           cudaDeviceCanAccessPeer(&ok, c->devices[a], c->devices[b]);
@@ -541,8 +663,12 @@ int pst_step(pst_ctx* c, const pst_batch* batch) {
       PST_CUDA(cudaEventRecord(c->pin_ev2[pi], SL->stream));
     }
     c->n_fed += 1;
-    if (c->mode == MODE_PIPE) pipe_step(c);
-    else np_step(c);
+    if (c->mode == MODE_PIPE) {
+      if (c->mapping == PST_MAP_FS_BKS) fsbks_step(c);
+      else pipe_step(c);
+    } else {
+      np_step(c);
+    }
   });
 }
 
@@ -550,6 +676,7 @@ int pst_set_hybrid(pst_ctx* c, int64_t switch_epoch) {
   if (!c) return PST_E_INVALID;
   return guard(c, [&] {
     if (c->mode == MODE_NP) throw StateError("already switched to non-pipelined training");
+    if (c->mapping == PST_MAP_FS_BKS) throw Unsupported("hybrid training with the FS/BKS mapping");
     const int64_t spe = c->hp.steps_per_epoch > 0 ? c->hp.steps_per_epoch : 1;
     c->n_p = switch_epoch < 0 ? INT64_MAX : switch_epoch * spe;
     if (c->n_p < c->n_fed) c->n_p = c->n_fed;  // switch at the next step
@@ -580,10 +707,12 @@ int pst_weights(pst_ctx* c, uint32_t what, float* out, int64_t cap, int64_t* n) 
     PST_CHECK_ARG(cap >= need, "output buffer too small");
     sync_all(c);
     int64_t o = 0;
+    // the master weights and momentum live with the backward stage (FS/BKS mapping: BKS_s)
+    auto master = [&](size_t i) -> Stage* { return i < c->bks.size() ? c->bks[i].get() : c->stages[i].get(); };
     if (what & PST_W_PARAMS)
-      for (auto& S : c->stages) { S->read_params(out + o, nullptr); o += S->n_params; }
+      for (size_t i = 0; i < c->stages.size(); ++i) { master(i)->read_params(out + o, nullptr); o += master(i)->n_params; }
     if (what & PST_W_MOMENTUM)
-      for (auto& S : c->stages) { S->read_params(nullptr, out + o); o += S->n_params; }
+      for (size_t i = 0; i < c->stages.size(); ++i) { master(i)->read_params(nullptr, out + o); o += master(i)->n_params; }
     if (what & PST_W_BNSTATS) {
       std::vector<float> mv;
       for (auto& S : c->stages) S->read_bnstats(mv);
@@ -613,7 +742,8 @@ int pst_versions(pst_ctx* c, int64_t* v, int32_t cap) {
   return guard(c, [&] {
     PST_CHECK_ARG(cap >= (int32_t)c->stages.size(), "cap");
     sync_all(c);
-    for (size_t i = 0; i < c->stages.size(); ++i) v[i] = c->stages[i]->read_version();
+    for (size_t i = 0; i < c->stages.size(); ++i)
+      v[i] = (i < c->bks.size() ? c->bks[i] : c->stages[i])->read_version();
   });
 }
 
@@ -639,12 +769,17 @@ int pst_sync(pst_ctx* c) {
 
 void pst_destroy(pst_ctx* c) {
   if (!c) return;
-  for (auto& S : c->stages) {
-    cudaSetDevice(S->dev);
-    cudaStreamSynchronize(S->stream);
-  }
-  for (auto& m : c->graphs)
-    for (auto& kv : m) cudaGraphExecDestroy(kv.second.exec);
+  for (auto* v : {&c->stages, &c->bks})
+    for (auto& S : *v) {
+      cudaSetDevice(S->dev);
+      cudaStreamSynchronize(S->stream);
+    }
+  for (auto* gv : {&c->graphs, &c->graphs_b})
+    for (auto& m : *gv)
+      for (auto& kv : m) cudaGraphExecDestroy(kv.second.exec);
+  for (auto e : c->bdone) cudaEventDestroy(e);
+  for (auto e : c->wev) cudaEventDestroy(e);
+  c->bks.clear();
   for (auto e : c->done) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
     if (c->pin_x[i]) cudaFreeHost(c->pin_x[i]);
@@ -728,6 +863,7 @@ int pst_profile(pst_ctx* c, int32_t enable) {
 int pst_stage_timing(pst_ctx* c, int32_t enable) {
   if (!c) return PST_E_INVALID;
   return guard(c, [&] {
+    if (c->mapping == PST_MAP_FS_BKS) throw Unsupported("per-stage timing with the FS/BKS mapping");
     sync_all(c);
     if (c->st_beg.empty()) {
       for (size_t i = 0; i < c->stages.size(); ++i) {

@@ -111,6 +111,12 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
     const size_t out_el = (size_t)B * li.Ho * li.Wo * li.Coutp;
     const bool last_net = (l == (int)net.layers.size() - 1);
     const size_t before_ring = bytes_total;
+    b.y_bytes = li.spec.bn ? out_el * sizeof(act_t) : 0;
+    b.z_bytes = last_net ? out_el * sizeof(float) : out_el * sizeof(act_t);
+    b.p_bytes = li.spec.pool == PST_POOL_MAX2 ? out_el / 4 * sizeof(act_t)
+              : li.spec.pool == PST_POOL_GAP ? (size_t)B * li.Coutp * sizeof(act_t) : 0;
+    b.arg_bytes = li.spec.pool == PST_POOL_MAX2 ? out_el / 4 : 0;
+    b.saved_bytes = li.spec.bn ? 2 * li.Coutp * sizeof(float) : 0;
     for (int r = 0; r < R; ++r) {
       if (li.spec.bn) b.y.push_back(alloc<act_t>(out_el, false));
       if (last_net) b.zf.push_back(alloc<float>(out_el));
@@ -491,6 +497,29 @@ void Stage::enqueue_backward(int64_t mb, int dpar, cudaStream_t st) {
     PST_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
   }
   if (!skip("sgd")) sgd_update(sgd_, st);
+}
+
+// ------------------------------------------------------------------ FS/BKS mapping
+void Stage::copy_saved_to(const Stage& d, int64_t mb, cudaStream_t st) const {
+  const int ss = (int)(mb % R), ds = (int)(mb % d.R);
+  PST_CUDA(cudaMemcpyAsync(d.xin_[mb % d.Rin], xin_[mb % Rin], input_bytes(), cudaMemcpyDefault, st));
+  if (starts_mid())
+    PST_CUDA(cudaMemcpyAsync(d.xin2_[mb % d.Rin], xin2_[mb % Rin], input2_bytes(), cudaMemcpyDefault, st));
+  for (int l = l0; l < l1; ++l) {
+    const LayerBufs& a = L_[l - l0];
+    const LayerBufs& b = d.L_[l - l0];
+    if (a.y_bytes) PST_CUDA(cudaMemcpyAsync(b.y[ds], a.y[ss], a.y_bytes, cudaMemcpyDefault, st));
+    if (!a.z.empty()) PST_CUDA(cudaMemcpyAsync(b.z[ds], a.z[ss], a.z_bytes, cudaMemcpyDefault, st));
+    if (!a.zf.empty()) PST_CUDA(cudaMemcpyAsync(b.zf[ds], a.zf[ss], a.z_bytes, cudaMemcpyDefault, st));
+    if (a.p_bytes) PST_CUDA(cudaMemcpyAsync(b.p[ds], a.p[ss], a.p_bytes, cudaMemcpyDefault, st));
+    if (a.arg_bytes) PST_CUDA(cudaMemcpyAsync(b.arg[ds], a.arg[ss], a.arg_bytes, cudaMemcpyDefault, st));
+    if (a.saved_bytes) PST_CUDA(cudaMemcpyAsync(b.saved[ds], a.saved[ss], a.saved_bytes, cudaMemcpyDefault, st));
+  }
+}
+
+void Stage::copy_weights_from(const Stage& src, cudaStream_t st) {
+  PST_CUDA(cudaMemcpyAsync(w_, src.w_, n_params * sizeof(float), cudaMemcpyDefault, st));
+  build_shadows(sgd_, st);   // the forward copy's weight shadows (hi/lo planes) from the new weights
 }
 
 // ------------------------------------------------------------------ host readback

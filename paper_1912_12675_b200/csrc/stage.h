@@ -24,6 +24,7 @@ struct LayerBufs {
   int ksplit = 1;
   double* stats = nullptr;       // forward BN sums [Coutp][2]
   double* sums = nullptr;        // backward sums [Coutp][2]
+  size_t y_bytes = 0, z_bytes = 0, p_bytes = 0, arg_bytes = 0, saved_bytes = 0;   // per ring slot
   act_t* sh_fwd = nullptr;       // [k*k][Coutp][Cinp]
   act_t* sh_bwd = nullptr;       // [k*k][Cinp][Coutp]
 };
@@ -68,6 +69,11 @@ class Stage {
   int32_t* label_slot(int64_t mb) const { return label_ring_ + (mb % label_ring_n_) * batch_; }
 
   void set_n_p(int64_t n_p);
+  // The paper's FS/BKS mapping (pst.h PST_MAP_FS_BKS): the forward copy of a stage hands the saved
+  // forward state of mini-batch mb to the backward copy, and the backward copy forwards
+  // its new weights to the forward copy.  Both enqueue on `st` (the caller orders them).
+  void copy_saved_to(const Stage& dst, int64_t mb, cudaStream_t st) const;
+  void copy_weights_from(const Stage& src, cudaStream_t st);
   // Synchronous host copies (call only when the stream is idle).
   void read_params(float* out_params, float* out_mom) const;   // canonical stage block
   void read_bnstats(std::vector<float>& mean_var) const;       // per BN layer: mean[C], var[C]

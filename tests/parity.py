@@ -338,9 +338,10 @@ def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, sp
     data = W.batches(net.in_shape, B, N, seed=seed + 100)
     lr_np = lr[-1] if lr_np is None else lr_np
     hp = hparams(lr, K, lr_np, mom, wd, milestones, 0.1, spe)
-    skw = dict(solver_kw or {})        # solver / nesterov / lr_policy / inv_gamma / inv_power
+    skw = dict(solver_kw or {})        # solver / nesterov / lr_policy / inv_gamma / inv_power (/ mapping)
     for k, v in skw.items():
-        setattr(hp, k, v)
+        if hasattr(hp, k):
+            setattr(hp, k, v)
     snap = (True if check is None else set(check)) if per_step else False
     ref = oracle_run(net, flat, ppv, data, hp, n_p=n_p, snapshot=snap, dropout_seed=dropout_seed)
     P = Parity(tag or _test_name())

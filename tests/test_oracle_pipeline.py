@@ -394,3 +394,38 @@ def test_speedup_formulas():
     for tn, tp, sp in [(2421, 1974, 1.23), (6745, 4090, 1.65), (13150, 7570, 1.73),
                        (27231, 14998, 1.81), (44814, 24640, 1.82)]:
         assert abs(tn / tp - sp) < 0.01
+
+
+@pytest.mark.parametrize("name,K", [("tiny_resnet", 1), ("tiny_resnet", 2), ("tiny_resnet", 3), ("tiny_cnn", 4),
+                                    ("tiny_resnet2_mid", 3)])
+def test_fs_bks_mapping_equals_versioned(name, K):
+    """Oracle C (the paper's 2K_p+1-accelerator mapping; SURVEY f-4) against Oracle A:
+    bitwise equal losses and weights (the mapping moves work between accelerators, not the math),
+    and the forward-version log equals the closed form of P:L75."""
+    if name == "tiny_resnet2_mid":
+        net, B, ppv = W.tiny_resnet(width=4, hw=8, n=2), 6, (2, 6)
+    else:
+        net, B, ppvs = NETS[name]
+        ppv = ppvs[K]
+    flat = W.init_params(net, seed=21)
+    data = W.batches(net.in_shape, B, 9, seed=22)
+    sa, bounds = make_stages(net, ppv)
+    sc, _ = make_stages(net, ppv)
+    p0 = split_params(net, flat, bounds)
+    hp = hp_for(K)
+    ra = Pl.run_versioned(sa, p0, data, hp)
+    rc = Pl.run_fs_bks(sc, p0, data, hp)
+    assert ra.losses == rc.losses
+    assert np.array_equal(flat_of(net, bounds, ra.params), flat_of(net, bounds, rc.params))
+    for t, s, kind, mb, ver in rc.version_log:
+        if kind == "F":
+            assert ver == max(0, mb - 2 * (K - 1 - s)), (t, s, mb, ver)
+        if kind == "B":
+            assert ver == mb
+    # 2K-1 accelerators busy in the steady state: per cycle K forwards and K backwards, the last
+    # stage doing both of the same mini-batch (P:L61, L67)
+    per_t = {}
+    for t, s, kind, mb, ver in rc.version_log:
+        per_t.setdefault(t, []).append((s, kind))
+    mid = per_t[2 * K]
+    assert sorted(mid) == sorted([(s, "F") for s in range(K)] + [(s, "B") for s in range(K)]) if len(data) > 2 * K else True
