@@ -39,7 +39,6 @@ struct WtArgs {
   int rows, n_mt, G, n_mgroups, BNw, n_ntiles, ksplit;
   int pl_grp, pl_all;
   int SB, St;                          // smem stages, TMEM A slots
-  int log2Wo, log2hw;                  // log2 of Wo and bh*Wo when both are powers of two, else -1
   int sets;                            // converter sets (2 or 3; compile-time in the kernel)
   uint32_t rawx_bytes, rawx_tx, rawd_bytes, b_bytes, stage_bytes, sboB;
   float* part;
@@ -201,6 +200,7 @@ __global__ void __launch_bounds__(wt_threads(SETS), 1)
     }
     const int nq = a.P16 / 4;
     const int unitsB = (a.BNw / 4) * nq;
+
     int sb = 0, slot = 0;
     uint32_t sbph = 0, slph = 0;
     int turn = 0;                               // set owning unit `it`
@@ -259,16 +259,7 @@ __global__ void __launch_bounds__(wt_threads(SETS), 1)
           float hv[16], lv[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            // pixel offset in the band: arithmetic when the unit's geometry is a power of two
-            // (every ResNet-CIFAR layer), else the shared table
-            const int p = h * 16 + i;
-            int pbv;
-            if (a.log2Wo >= 0) {
-              const int jj = p >> a.log2hw, py = (p >> a.log2Wo) & (a.bh - 1), px = p & (a.Wo - 1);
-              pbv = p < a.P ? ((jj * a.band_r + py * a.S) * a.band_c + px * a.S) * 4 : -1;
-            } else {
-              pbv = pixb[p];                         // broadcast shared load
-            }
+            const int pbv = pixb[h * 16 + i];       // broadcast shared load
             hv[i] = (rb[j] >= 0 && pbv >= 0) ? rawxf[rb[j] + pbv] : 0.f;
             lv[i] = tf32_lo(hv[i]);
           }
@@ -342,12 +333,6 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   if (Ho * Wo >= ptarget) { a.nb = 1; a.bh = std::max(1, std::min(Ho, ptarget / Wo)); }
   else { a.nb = std::max(1, std::min(N, ptarget / (Ho * Wo))); a.bh = Ho; }
   a.P = a.nb * a.bh * Wo;
-  {
-    auto lg = [](int v) { int l = 0; while ((1 << l) < v) ++l; return (1 << l) == v ? l : -1; };
-    a.log2Wo = lg(Wo);
-    a.log2hw = lg(a.bh * Wo);
-    if (a.log2Wo < 0 || a.log2hw < 0 || lg(a.bh) < 0) a.log2Wo = a.log2hw = -1;
-  }
   a.P16 = round_up(a.P, 16);
   if (a.P16 != 16 && a.P16 != 32 && a.P16 != 64) return false;
   a.band_r = (a.bh - 1) * S + k;

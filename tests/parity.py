@@ -323,7 +323,7 @@ def perturbed(flat):
 
 def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, spe=1 << 62,
              milestones=(), per_step=True, seed=5, check=None, deep=False, spread=True, solver_kw=None,
-             tag=None, dropout_seed=0):
+             tag=None, dropout_seed=0, emu=True):
     """Train the same seeded mini-batches through libpst (all stages on cuda:0, local mode)
     and through Oracle B; compare the weights after every compared step and after the drain
     (split measure, see the module docstring), the momentum buffers and BN running statistics
@@ -350,7 +350,7 @@ def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, sp
     if spread:
         # the oracle's own sensitivity (AMB-21d) and a float32 emulation of the same arithmetic (AMB-21e)
         refp = oracle_run(net, perturbed(flat), ppv, data, hp, n_p=n_p, snapshot=snap, dropout_seed=dropout_seed)
-        refe = oracle_run(net, flat, ppv, data, hp, n_p=n_p, snapshot=snap, dropout_seed=dropout_seed, emu=True)
+        refe = oracle_run(net, flat, ppv, data, hp, n_p=n_p, snapshot=snap, dropout_seed=dropout_seed, emu=emu)
         snaps = ref.snapshots if ref.snapshots is not None else {}
         idx = range(len(snaps)) if isinstance(snaps, list) else snaps.keys()
         for t in idx:
@@ -391,7 +391,7 @@ def run_both(pst, net, ppv, B, N, lr, lr_np=None, mom=0.9, wd=1e-4, n_p=None, sp
 
 
 def run_segments(pst, net, ppv, B, seg_lens, lr, lr_np=None, mom=0.9, wd=1e-4, seed=5, deep=True, tag=None,
-                 spread=True):
+                 spread=True, emu=True):
     """Segment ("shadowing") parity for trajectories that are chaotic (reading AMB-21c).
 
     The GPU trains sum(seg_lens) mini-batches; after each segment the pipe is drained
@@ -420,7 +420,8 @@ def run_segments(pst, net, ppv, B, seg_lens, lr, lr_np=None, mom=0.9, wd=1e-4, s
         sp = {}
         if spread:   # the oracle's own sensitivity over this segment and its float32 emulation
             sp = allowances(oracle_spreads(net, ppv, ref, oracle_run(net, perturbed(w_state), ppv, seg, hp, mom0=v_state)),
-                            oracle_spreads(net, ppv, ref, oracle_run(net, w_state, ppv, seg, hp, mom0=v_state, emu=True)))
+                            oracle_spreads(net, ppv, ref, oracle_run(net, w_state, ppv, seg, hp, mom0=v_state, emu=True))
+                            if emu else None)
         for x, y in seg:
             pipe.step(x, y)
         pipe.flush()
