@@ -318,18 +318,34 @@ int tile_n16(int C, int cap) {
 
 }  // namespace
 
+static bool wgrad_ts_plan_p(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad,
+                            int num_sm, int ptarget, WtArgs& a);
+
+// Pixels per unit: 32 by default; 16 when 32-pixel units leave fewer than 3 TMEM A slots and 16-pixel
+// units do not (the 32-channel ResNet-CIFAR layers: 3 M tiles at N = 32 fit 2 slots of 32 pixels but
+// 4 of 16; measured g2 wgrad 19.9 -> 13.7 us, profiles/r2_wgrad_knobs.txt).
 bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad, int num_sm,
                    void* out) {
   if (pst_knob("PST_NOTS", 0)) return false;
-  WtArgs a{};
+  static const int forced = pst_knob("PST_WT_PTARGET", 0);   // experiment: fixed pixels per unit
+  WtArgs a{}, b{};
+  bool ok = wgrad_ts_plan_p(N, H, W, Cinp, Ho, Wo, Coutp, k, S, pad, num_sm, forced ? forced : 32, a);
+  if (!forced && ok && a.St < 3 && wgrad_ts_plan_p(N, H, W, Cinp, Ho, Wo, Coutp, k, S, pad, num_sm, 16, b) &&
+      b.St >= 3 && b.G == a.G)
+    a = b;
+  if (ok && out) *reinterpret_cast<WtArgs*>(out) = a;
+  return ok;
+}
+
+static bool wgrad_ts_plan_p(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int k, int S, int pad,
+                            int num_sm, int ptarget, WtArgs& a) {
+  a = WtArgs{};
   a.N = N; a.H = H; a.W = W; a.Cinp = Cinp; a.Ho = Ho; a.Wo = Wo; a.Coutp = Coutp;
   a.k = k; a.S = S; a.pad = pad;
   a.rows = k * k * Cinp;
   a.n_mt = ceil_div(a.rows, 128);
   a.BNw = tile_n16(Coutp, 128);
   a.n_ntiles = Coutp / a.BNw;
-  // pixels per unit (PST_WT_PTARGET experiments: 64 halves the per-unit hand-offs, needs G = 1)
-  static const int ptarget = pst_knob("PST_WT_PTARGET", 32);
   if (Ho * Wo >= ptarget) { a.nb = 1; a.bh = std::max(1, std::min(Ho, ptarget / Wo)); }
   else { a.nb = std::max(1, std::min(N, ptarget / (Ho * Wo))); a.bh = Ho; }
   a.P = a.nb * a.bh * Wo;
@@ -340,7 +356,8 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   if (a.band_c * kEPC > 256 || a.band_r > 256) return false;
   // M tiles per CTA: largest G with >= 2 TMEM slots
   a.G = 0;
-  for (int G = std::min(a.n_mt, 4); G >= 1; --G) {
+  static const int gmax = pst_knob("PST_WT_GMAX", 4);   // experiment: cap on M tiles per CTA
+  for (int G = std::min(std::min(a.n_mt, 4), std::max(1, gmax)); G >= 1; --G) {
     const int slots = (512 - G * a.BNw) / (G * 2 * a.P16);
     if (slots >= 2) { a.G = G; a.St = std::min(kWtMaxSlots, slots); break; }
   }
@@ -364,7 +381,8 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   static const int max_sets = pst_knob("PST_WT_SETS", 3);
   // (measured: g1 wgrad 24.2 -> 21.3 us with 3 sets; the 576-row g3 gets slower, so only the
   // small-row layers take it)
-  a.sets = (max_sets >= 3 && a.St >= 3 && a.SB >= 3 && a.rows <= 256) ? 3 : 2;
+  static const int sets3_rows = pst_knob("PST_WT_SETS3_ROWS", 256);   // experiment: row limit for 3 sets
+  a.sets = (max_sets >= 3 && a.St >= 3 && a.SB >= 3 && a.rows <= sets3_rows) ? 3 : 2;
   a.n_mgroups = ceil_div(a.n_mt, a.G);
   a.ny = ceil_div(Ho, a.bh);
   a.n_units = ceil_div(N, a.nb) * a.ny;
@@ -375,7 +393,6 @@ bool wgrad_ts_plan(int N, int H, int W, int Cinp, int Ho, int Wo, int Coutp, int
   if (ks_max > 0) a.ksplit = std::min(a.ksplit, ks_max);
   static const int ks_big = pst_knob("PST_WT_KSPLIT_MAX_BIG", 0);
   if (ks_big > 0 && a.rows > 256) a.ksplit = std::min(a.ksplit, ks_big);   // the many-row (64-channel) layers only
-  if (out) *reinterpret_cast<WtArgs*>(out) = a;
   return true;
 }
 

@@ -5,8 +5,9 @@ runtime; the stage time of a K-GPU pipeline is the time of its 
 the speedup is bounded by sum(costs) / (K * max stage cost).  Given the measured cost of every
 weighted layer (forward + backward + update work on the B200, see b200_costs.json) this module
 finds the partition-point vector (PPV) that minimises the maximum stage cost over the
-allowed boundaries (ResNet: block boundaries, AMB-14) by dynamic programming -- host logic only,
-no method arithmetic.
+allowed boundaries by dynamic programming -- host logic only, no method arithmetic.  Since round 2
+every layer boundary is allowed, including points inside a residual block (two-tensor registers,
+SURVEY f-2, reading AMB-14).
 """
 from __future__ import annotations
 
@@ -41,11 +42,18 @@ def resnet_layer_costs(net: NetSpec, table: Dict) -> List[float]:
     return c
 
 
-def resnet_boundaries(net: NetSpec) -> List[int]:
-    """Allowed PPV entries of an option-A ResNet: after the first conv or after a residual block
-    (odd weighted-layer numbers 1 + 2k below L), reading AMB-14."""
+def resnet_block_boundaries(net: NetSpec) -> List[int]:
+    """PPV entries of an option-A ResNet between residual blocks: after the first conv or after a
+    block (odd weighted-layer numbers 1 + 2k below L)."""
     L = weighted_layer_count(net)
     return [p for p in range(1, L) if p % 2 == 1]
+
+
+def resnet_boundaries(net: NetSpec) -> List[int]:
+    """Allowed PPV entries: every weighted layer 1..L-1 (mid-block points carry the block input
+    too, SURVEY f-2, reading AMB-14; every block of these nets has two layers, so a partition has
+    at most one point inside any block)."""
+    return list(range(1, weighted_layer_count(net)))
 
 
 def stage_costs(costs: Sequence[float], ppv: Sequence[int]) -> List[float]:
