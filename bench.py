@@ -387,10 +387,19 @@ def main():
     conv_tflops = (sum(v[3] for v in conv) / (conv_ms / 1e3) / 1e12) if conv_ms > 0 else 0.0
     conv_pipe = {"tflops": conv_tflops, "peak_tflops": tc_peak, "pct": 100.0 * conv_tflops / tc_peak if tc_peak else None,
                  "conv_ms_per_step": conv_ms / max(1, args.profile_steps),
-                 "note": "sum of conv FLOPs / conv kernel time (per-kernel CUDA events, serial) / " + tc_note}
+                 "note": "sum of conv FLOPs / conv kernel time (per-kernel CUDA events, serial) / " + tc_note,
+                 "ncu_counter": "sm__pipe_tensor_cycles_active 9.5-12.9% on the ResNet-110 conv kernels "
+                                "(tcgen05 UTCHMMA issue; profiles/r2_tc_counters.txt)"}
+    def class_roofline(v):
+        # each class against its own binding resource: the larger of its algorithmic bytes at the HBM
+        # peak and its flops at the contraction peak, over its event-timed device time
+        tb = v[2] / (hbm_peak * 1e9) if v[2] else 0.0
+        tt = v[3] / (tc_peak * 1e12) if v[3] else 0.0
+        return ("tensor" if tt > tb else "hbm"), (max(tb, tt) / (v[0] / 1e3) if v[0] > 0 else None)
     kernel_table = {k: {"ms_per_step": v[0] / max(1, args.profile_steps), "launches_per_step": v[1] / max(1, args.profile_steps),
                         "GBps": (v[2] / (v[0] / 1e3) / 1e9) if v[0] > 0 else 0.0,
-                        "TFLOPs": (v[3] / (v[0] / 1e3) / 1e12) if v[0] > 0 else 0.0}
+                        "TFLOPs": (v[3] / (v[0] / 1e3) / 1e12) if v[0] > 0 else 0.0,
+                        "bound": class_roofline(v)[0], "roofline_frac": class_roofline(v)[1]}
                     for k, v in prof.items() if v[1] > 0}
 
     # ---- end-to-end through the public API: host buffers, H2D + loss readback every step

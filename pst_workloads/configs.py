@@ -5,9 +5,10 @@ Table 5), otherwise the roofline-balanced block-boundary PPVs of
 SURVEY.md Appendix A -- except ResNet-110/362, whose PPVs come from the
 profile-driven balancer (balance.py) on the per-layer costs
 measured on the B200 (b200_costs.json, round 2), over every layer boundary including the
-mid-block ones (SURVEY f-2): the paper's hand placement (37) leaves its 2-GPU pipeline at 0.85
-of the ideal speedup with B200 layer costs, the balanced (48) at 0.997; K=8 0.962 with mid-block
-points against 0.928 at block boundaries only (tests/test_balance.py); `paper_ppv` keeps the paper's.  Hyperparameters: Appendix A/B of the paper
+mid-block ones (SURVEY f-2), with the per-group costs fitted to the per-stage step times measured
+inside the pipeline: ResNet-110 K=2 (45), K=4 (22,45,75), K=8 (10,21,32,45,60,75,92) allow 1.00 /
+0.98 / 0.97 of the ideal speedup by the cost model (the paper's hand placement (37): 0.85);
+`paper_ppv` keeps the paper's.  Hyperparameters: Appendix A/B of the paper
 (PAPER.md L282-306): momentum 0.9; weight decay 5e-4 (LeNet, VGG), 4e-3
 (AlexNet), 1e-4 (ResNet); base lr 0.01 (LeNet), 0.001 (AlexNet), 0.1 (VGG,
 ResNet); the pipelined ResNet's stale stages use the Table 7 BKS_2 rate
@@ -56,10 +57,10 @@ CONFIGS = {
                     {1: (), 2: (2,), 4: (2, 4, 7), 8: (1, 2, 4, 6, 7, 9, 10)},
                     0.1, 0.1, 0.9, 5e-4, 100),
     "resnet110": Config("resnet110", "resnet110", 128,
-                        {1: (), 2: (48,), 4: (23, 48, 79), 8: (11, 22, 33, 47, 63, 79, 94)},
+                        {1: (), 2: (45,), 4: (22, 45, 75), 8: (10, 21, 32, 45, 60, 75, 92)},
                         0.1, 0.001, 0.9, 1e-4, 100, milestones=(100, 150), paper_ppv={2: (37,)}),
     "resnet362": Config("resnet362", "resnet362", 128,
-                        {1: (), 2: (158,), 4: (74, 158, 261), 8: (37, 74, 111, 158, 210, 261, 311)},
+                        {1: (), 2: (148,), 4: (70, 148, 248), 8: (35, 70, 105, 148, 197, 247, 304)},
                         0.1, 0.001, 0.9, 1e-4, 20, milestones=(100, 150),
                         steps_per_epoch=5, hybrid_epoch=2, paper_ppv={2: (121,)}),
 }

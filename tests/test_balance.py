@@ -62,5 +62,5 @@ def test_resnet110_balance_numbers():
     net = W.nets.by_name("resnet110")
     costs = Bl.resnet_layer_costs(net, Bl.load_cost_table())
     assert len(costs) == 111
-    assert Bl.balance_efficiency(costs, (48,)) > 0.95 > Bl.balance_efficiency(costs, (37,))
+    assert Bl.balance_efficiency(costs, (45,)) > 0.95 > Bl.balance_efficiency(costs, (37,))
     assert Bl.balance_efficiency(costs, W.CONFIGS["resnet110"].ppv[8]) > 0.9

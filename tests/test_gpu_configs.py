@@ -86,13 +86,13 @@ def test_resnet110_b128_k2(pst):
 
 
 def test_resnet110_b128_k2_balanced_table7(pst):
-    """bench.py's 2-GPU workload exactly: ResNet-110, batch 128, the profile-balanced PPV (48) (a mid-block point) and
+    """bench.py's 2-GPU workload exactly: ResNet-110, batch 128, the profile-balanced PPV (45) and
     the Table-7 rate vector [0.001, 0.1] -- the configuration the K=2 bench line times."""
     _run(pst, "resnet110", 2, 128, 6, check={3, 5}, deep=True, spread=True)
 
 
 def test_resnet110_k2_balanced_ppv(pst):
-    """bench.py's 2-GPU partition: the profile-balanced PPV (48) (pst_workloads/balance.py; inside a group-2 block)."""
+    """bench.py's 2-GPU partition: the profile-balanced PPV (45) (pst_workloads/balance.py)."""
     _run(pst, "resnet110", 2, 32, 4, check={3}, lr=0.001, deep=True, spread=True)
 
 

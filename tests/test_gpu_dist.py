@@ -149,7 +149,7 @@ def test_dist_k4_tiny_cnn(gpu):
 
 def test_dist_k2_resnet110_b128(gpu):
     """bench.py's 2-GPU workload through the distributed path: ResNet-110, batch 128, the balanced
-    PPV (48) -- a point inside a block, so the block input and shortcut gradient cross NCCL too --, Table 7's rate vector [0.001, 0.1]; 4 mini-batches (mini-batch 3's stage-0
+    PPV (45), Table 7's rate vector [0.001, 0.1]; 4 mini-batches (mini-batch 3's stage-0
     forward reads a stale version).  Deep BN net: beta per stage (AMB-21b)."""
     cfg = W.CONFIGS["resnet110"]
     _check(gpu, dict(net="resnet_cifar", net_kw=dict(depth=110), ppv=list(cfg.ppv[2]), B=128, N=4, seed=31,

@@ -6,8 +6,10 @@ import csv, os, shutil, subprocess, sys
 
 run, tag = sys.argv[1], sys.argv[2]
 P = "profiles"
-for src, dst in [("bench.json", "bench.json"), ("bench2.json", "bench_repeat.json"),
-                 ("bench_ref.json", "bench_reference.json"), ("tg.log", "pytest_gpu.log"), ("smoke.log", "smoke.log")]:
+for src, dst in [("bench.json", "bench.json"), ("bench2.json", "bench_repeat.json"), ("bench_repeat.json", "bench_repeat.json"),
+                 ("bench_ref.json", "bench_reference.json"), ("bench_reference.json", "bench_reference.json"),
+                 ("bench_n2_shared_gpu.json", "bench_n2_shared_gpu.json"), ("stage_times.jsonl", "stage_times.jsonl"),
+                 ("tg.log", "pytest_gpu.log"), ("smoke.log", "smoke.log")]:
     if os.path.exists(os.path.join(run, src)):
         shutil.copy(os.path.join(run, src), os.path.join(P, f"{tag}_{dst}"))
 rows = list(csv.reader(open(os.path.join(run, "traffic.csv"))))
@@ -25,10 +27,12 @@ KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
         "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tensor_subpipe_hmma.sum", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "launch__grid_size",
         "launch__block_size", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
         "sm__warps_active.avg.pct_of_peak_sustained_active"]
-for name in ("wgrad", "ts"):
+for name in ("wgrad", "ts", "bn_apply"):
     rep = os.path.join(run, f"prof_{name}.ncu-rep")
     if not os.path.exists(rep):
         continue
