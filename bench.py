@@ -306,6 +306,9 @@ def main():
     # untimed spin-up: about 1.5 s more of steps so a fresh box's clocks and caches settle (the
     # first bench on a new box otherwise sometimes reads 20-50% slow); the count is agreed on
     # by all ranks, whose stages exchange activations every step
+    # clocks: sampled from the start of the spin-up through the end of the timed region (the timed
+    # region alone is ~0.1 s, shorter than nvidia-smi's sampling period)
+    clocks = ClockSampler(local)
     n_spin = int(max_over_ranks(float(min(2000, int(args.spin_seconds / max(per_step, 1e-4))))))
     for i in range(n_spin):
         pipe.step(*dev[(warm + i) % n_pool])
@@ -317,7 +320,6 @@ def main():
     barrier()
 
     # ---- device-timed region: inputs resident in HBM
-    clocks = ClockSampler(local)
     l0 = pipe.launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -443,6 +445,11 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.cpu_sample)
 
+    if shared:
+        placement = ("all ranks on cuda:0, NCCL socket transport (PST_BENCH_SHARE_GPU=1): a functional check "
+                     "of the N-rank path, not a throughput measurement")
+    else:
+        placement = "one process per GPU, NCCL send/recv" if world > 1 else "one GPU"
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "img/s", "n_gpus": world, "steps": args.steps,
@@ -452,7 +459,8 @@ def main():
             "config": {"workload": f"{cfg.net}_cifar10_b{B}_pp{K}", "model": cfg.net, "global_batch": B,
                        "stages": K, "ppv": list(ppv), "parallelism": f"pp{K}" if K > 1 else "none",
                        "precision": "fp32 storage, 3xTF32 tensor-core products (" + pst.build_info() + ")",
-                       "l2": "inputs larger than L2 (saved-activation ring >> 126 MB)",
+                       "l2": "inputs larger than L2 (saved forward state ~1 GB per mini-batch >> 126 MB)",
+                       "placement": placement,
                        "lr_per_stage": lr},
             "clocks": clk, "gpu_launches": launches, "roofline": roofline, "conv_tensor_pipe": conv_pipe,
             "kernels": kernel_table,
