@@ -283,6 +283,11 @@ int64_t pst_param_count(const pst_net* net);
 int pst_schedule(int32_t K, int32_t s, int64_t t, int64_t n_total,
                  int64_t* bwd_mb, int64_t* fwd_mb, int64_t* fwd_version);
 
+/* Ring sizes libpst uses for stage s of a K-stage pipeline (host only): *saved = slots of saved
+ * forward state (>= the paper's 2(K-s)-1), *input = slots of the received-activation ring
+ * (>= 2(K-s)+1 for s > 0), both divisors of the graph-key period *period = 2K+2. */
+int pst_ring_slots(int32_t K, int32_t s, int32_t* saved, int32_t* input, int32_t* period);
+
 /* Library build string (arch, compute dtype). */
 const char* pst_build_info(void);
 

@@ -95,6 +95,7 @@ def lib():
         "pst_schedule": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, P(C.c_int64),
                                    P(C.c_int64), P(C.c_int64)]),
         "pst_build_info": (C.c_char_p, []),
+        "pst_ring_slots": (C.c_int, [C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32), P(C.c_int32)]),
         "pst_launches": (C.c_int, [C.c_void_p, P(C.c_int64)]),
         "pst_profile": (C.c_int, [C.c_void_p, C.c_int32]),
         "pst_stage_timing": (C.c_int, [C.c_void_p, C.c_int32]),
@@ -165,6 +166,13 @@ def schedule(K: int, s: int, t: int, n_total: int = -1):
     b, f, v = C.c_int64(), C.c_int64(), C.c_int64()
     _check(lib().pst_schedule(K, s, t, n_total, C.byref(b), C.byref(f), C.byref(v)))
     return b.value, f.value, v.value
+
+
+def ring_slots(K: int, s: int):
+    """(saved-state slots, input-ring slots, graph-key period) of stage s (pst_ring_slots)."""
+    a, b, c = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(lib().pst_ring_slots(K, s, C.byref(a), C.byref(b), C.byref(c)))
+    return a.value, b.value, c.value
 
 
 def partition_ranges(net, ppv):

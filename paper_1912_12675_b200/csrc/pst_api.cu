@@ -917,6 +917,14 @@ int pst_memory(pst_ctx* c, int32_t stage, int64_t* out, int32_t cap) {
   });
 }
 
+int pst_ring_slots(int32_t K, int32_t s, int32_t* saved, int32_t* input, int32_t* period) {
+  if (K < 1 || s < 0 || s >= K || !saved || !input || !period) return PST_E_INVALID;
+  *saved = ring_saved(K, s);
+  *input = ring_input(K, s);
+  *period = ring_period(K);
+  return PST_OK;
+}
+
 const char* pst_build_info(void) {
   return "libpst sm_100a act=" PST_ACT_NAME " tcgen05+TMA implicit-GEMM conv, NCCL " ;
 }

@@ -77,3 +77,22 @@ def test_schedule_matches_closed_form(pst, K):
 def test_nccl_unique_id(pst):
     a = pst.nccl_unique_id()
     assert len(a) == 128 and any(a)
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 5, 8, 10])
+def test_ring_slots(pst, K):
+    """Saved-state rings hold at least the paper's 2(K-s)-1 mini-batches, input rings of
+    stages s > 0 at least 2(K-s)+1 (the neighbour's copy of the next mini-batch lands while the stage
+    still reads b..f), every size divides the graph-key period 2K+2, and each is the smallest such
+    divisor (no memory beyond what the period forces)."""
+    P = 2 * K + 2
+    for s in range(K):
+        saved, inp, period = pst.ring_slots(K, s)
+        assert period == P and P % saved == 0 and P % inp == 0
+        need_s = 2 * (K - s) - 1
+        need_i = need_s if s == 0 else 2 * (K - s) + 1
+        assert saved >= need_s and inp >= need_i
+        assert all(P % d for d in range(need_s, saved))
+        assert all(P % d for d in range(need_i, inp))
+    assert pst.ring_slots(1, 0)[:2] == (1, 1)
+    assert [pst.ring_slots(8, s)[0] for s in range(8)] == [18, 18, 18, 9, 9, 6, 3, 1]
