@@ -136,6 +136,47 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
                          const StepPlan& next_stage, cudaStream_t st) {
   Stage* S = c->stage(s);
   const int K = c->K;
+  // distributed mode: which messages this step exchanges with each neighbour (both ends of a pair
+  // derive the same answer from the same plans)
+  const bool send_f = c->dist && p.fwd_mb >= 0 && s < K - 1;
+  const bool recv_f = c->dist && s > 0 && prev_stage.fwd_mb >= 0;
+  const bool send_b = c->dist && p.bwd_mb >= 0 && s > 0;
+  const bool recv_b = c->dist && s < K - 1 && next_stage.bwd_mb >= 0;
+  auto exchange_b = [&](cudaStream_t cs) {   // error of b to s-1, error of the next stage's b from s+1
+    PST_NCCL(ncclGroupStart());
+    if (send_b) {
+      PST_NCCL(ncclSend(S->dgrad_out(), S->input_bytes(), ncclUint8, s - 1, c->comm, cs));
+      if (S->starts_mid()) PST_NCCL(ncclSend(S->sgrad_out(), S->sgrad_bytes(), ncclUint8, s - 1, c->comm, cs));
+    }
+    if (recv_b) {
+      const int par = (int)(next_stage.bwd_mb & 1);
+      PST_NCCL(ncclRecv(S->dbuf(par), S->output_bytes(), ncclUint8, s + 1, c->comm, cs));
+      if (S->ends_mid()) PST_NCCL(ncclRecv(S->dbuf2(par), S->dbuf2_bytes(), ncclUint8, s + 1, c->comm, cs));
+    }
+    PST_NCCL(ncclGroupEnd());
+  };
+  auto exchange_f = [&](cudaStream_t cs) {   // activation of f to s+1, the previous stage's f from s-1
+    PST_NCCL(ncclGroupStart());
+    if (send_f) {
+      const int64_t f = p.fwd_mb;
+      PST_NCCL(ncclSend(S->output_slot(f), S->output_bytes(), ncclUint8, s + 1, c->comm, cs));
+      if (S->ends_mid()) PST_NCCL(ncclSend(S->block_out(f), S->block_out_bytes(), ncclUint8, s + 1, c->comm, cs));
+    }
+    if (recv_f) {
+      const int64_t f = prev_stage.fwd_mb;
+      PST_NCCL(ncclRecv(S->input_slot(f), S->input_bytes(), ncclUint8, s - 1, c->comm, cs));
+      if (S->starts_mid())
+        PST_NCCL(ncclRecv(S->input2_slot(f), S->input2_bytes(), ncclUint8, s - 1, c->comm, cs));
+    }
+    PST_NCCL(ncclGroupEnd());
+  };
+  // With comm overlap (default) the error exchange runs on the stage's communication stream while
+  // the forward pass computes, the activation exchange after it; the step joins that stream at its
+  // end, so the next step sees every received buffer.  The buffers the exchanges touch are disjoint
+  // from what the forward reads and writes (input ring slots f+1 vs f, dbuf parity of b+1 vs b).
+  static const bool overlap = pst_knob("PST_COMM_OVERLAP", 1) != 0;
+  const bool ov = c->dist && overlap;
+  bool forked = false;
   if (p.bwd_mb >= 0) {
     S->enqueue_backward(p.bwd_mb, (int)(p.bwd_mb & 1), st);
     if (s > 0 && !c->dist) {
@@ -145,6 +186,12 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
       if (S->starts_mid())   // mid-block register: the shortcut gradient goes back too
         PST_CUDA(cudaMemcpyAsync(D->dbuf2(par), S->sgrad_out(), S->sgrad_bytes(), cudaMemcpyDefault, st));
     }
+  }
+  if (ov && (send_b || recv_b)) {
+    PST_CUDA(cudaEventRecord(S->ev_cb, st));
+    PST_CUDA(cudaStreamWaitEvent(S->cstream, S->ev_cb, 0));
+    exchange_b(S->cstream);
+    forked = true;
   }
   if (p.fwd_mb >= 0) {
     S->enqueue_forward(p.fwd_mb, st);
@@ -156,35 +203,23 @@ static void enqueue_pipe(pst_ctx* c, int s, const StepPlan& p, const StepPlan& p
         PST_CUDA(cudaMemcpyAsync(D->input2_slot(f), S->block_out(f), S->block_out_bytes(), cudaMemcpyDefault, st));
     }
   }
-  if (c->dist) {
-    const bool send_f = p.fwd_mb >= 0 && s < K - 1;
-    const bool recv_f = s > 0 && prev_stage.fwd_mb >= 0;
-    const bool send_b = p.bwd_mb >= 0 && s > 0;
-    const bool recv_b = s < K - 1 && next_stage.bwd_mb >= 0;
-    if (send_f || recv_f || send_b || recv_b) {
-      PST_NCCL(ncclGroupStart());
-      if (send_f) {
-        const int64_t f = p.fwd_mb;
-        PST_NCCL(ncclSend(S->output_slot(f), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
-        if (S->ends_mid()) PST_NCCL(ncclSend(S->block_out(f), S->block_out_bytes(), ncclUint8, s + 1, c->comm, st));
-      }
-      if (recv_f) {
-        const int64_t f = prev_stage.fwd_mb;
-        PST_NCCL(ncclRecv(S->input_slot(f), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
-        if (S->starts_mid())
-          PST_NCCL(ncclRecv(S->input2_slot(f), S->input2_bytes(), ncclUint8, s - 1, c->comm, st));
-      }
-      if (send_b) {
-        PST_NCCL(ncclSend(S->dgrad_out(), S->input_bytes(), ncclUint8, s - 1, c->comm, st));
-        if (S->starts_mid()) PST_NCCL(ncclSend(S->sgrad_out(), S->sgrad_bytes(), ncclUint8, s - 1, c->comm, st));
-      }
-      if (recv_b) {
-        const int par = (int)(next_stage.bwd_mb & 1);
-        PST_NCCL(ncclRecv(S->dbuf(par), S->output_bytes(), ncclUint8, s + 1, c->comm, st));
-        if (S->ends_mid()) PST_NCCL(ncclRecv(S->dbuf2(par), S->dbuf2_bytes(), ncclUint8, s + 1, c->comm, st));
-      }
-      PST_NCCL(ncclGroupEnd());
+  if (ov) {
+    if (send_f || recv_f) {
+      PST_CUDA(cudaEventRecord(S->ev_cf, st));
+      PST_CUDA(cudaStreamWaitEvent(S->cstream, S->ev_cf, 0));
+      exchange_f(S->cstream);
+      forked = true;
     }
+    if (forked) {   // join: the step ends when its exchanges have completed
+      PST_CUDA(cudaEventRecord(S->ev_cj, S->cstream));
+      PST_CUDA(cudaStreamWaitEvent(st, S->ev_cj, 0));
+    }
+  } else if (c->dist && (send_f || recv_f || send_b || recv_b)) {
+    // one grouped exchange at the end of the step (PST_COMM_OVERLAP=0 experiment builds)
+    PST_NCCL(ncclGroupStart());
+    exchange_f(st);
+    exchange_b(st);
+    PST_NCCL(ncclGroupEnd());
   }
 }
 

@@ -55,6 +55,10 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
   PST_CUDA(cudaStreamCreateWithFlags(&wstream, cudaStreamNonBlocking));
   PST_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
   PST_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  PST_CUDA(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+  PST_CUDA(cudaEventCreateWithFlags(&ev_cb, cudaEventDisableTiming));
+  PST_CUDA(cudaEventCreateWithFlags(&ev_cf, cudaEventDisableTiming));
+  PST_CUDA(cudaEventCreateWithFlags(&ev_cj, cudaEventDisableTiming));
   const int B = batch;
   const int nsm = num_sms(dev);
   p_base = net.layers[l0].p_begin;
@@ -258,6 +262,9 @@ Stage::~Stage() {
   if (wstream) cudaStreamDestroy(wstream);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
+  if (cstream) { cudaStreamSynchronize(cstream); cudaStreamDestroy(cstream); }
+  for (cudaEvent_t e : {ev_cb, ev_cf, ev_cj})
+    if (e) cudaEventDestroy(e);
 }
 
 void Stage::set_n_p(int64_t n_p) {

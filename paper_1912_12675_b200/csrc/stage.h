@@ -92,6 +92,9 @@ class Stage {
   // concurrently with the dgrad chain of the layers below and joins before the update
   cudaStream_t wstream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // distributed mode: boundary exchanges on their own stream, overlapping the forward pass
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_cb = nullptr, ev_cf = nullptr, ev_cj = nullptr;
   bool is_first() const { return s == 0; }
   bool is_last() const { return l1 == (int)net_.layers.size(); }
 

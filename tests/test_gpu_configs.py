@@ -165,5 +165,5 @@ def test_resnet110_k2_segments_100_steps_table7(pst):
     and the weights after every drain compared (reading AMB-21c)."""
     cfg = W.CONFIGS["resnet110"]
     P = run_segments(pst, cfg.netspec(), cfg.ppv[2], 32, [5] * 20, cfg.lr_vector(2), mom=cfg.momentum,
-                     wd=cfg.weight_decay, emu=False).assert_ok()
+                     wd=cfg.weight_decay).assert_ok()
     assert len(P.ref.losses) == 100
