@@ -8,6 +8,7 @@ Where this spread exceeds a tenth of the tolerance no float32 implementation can
 exact trajectory step for step; the GPU parity tests switch to segment parity there.
 
     python tools/spread_curve.py resnet110 2 32 100 > profiles/r2_spread_curve_resnet110_k2_b32.jsonl
+    python tools/spread_curve.py resnet110 2 32 100 "" 0.001,0.01   # warm-up rates (lr/10)
 """
 from __future__ import annotations
 
@@ -25,11 +26,12 @@ from tests.parity import (flat_params, hparams, loss_errors, oracle_run, perturb
 
 def main():
     name, K, B, N = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
-    ppv = tuple(int(p) for p in sys.argv[5].split(",")) if len(sys.argv) > 5 else None
+    ppv = tuple(int(p) for p in sys.argv[5].split(",")) if len(sys.argv) > 5 and sys.argv[5] else None
+    lr_over = [float(v) for v in sys.argv[6].split(",")] if len(sys.argv) > 6 else None
     cfg = W.CONFIGS[name]
     net = cfg.netspec()
     ppv = cfg.ppv[K] if ppv is None else ppv
-    lr = cfg.lr_vector(K)
+    lr = cfg.lr_vector(K) if lr_over is None else lr_over
     flat = W.init_params(net, seed=5)
     data = W.batches(net.in_shape, B, N, seed=105)
     hp = hparams(lr, K, lr[-1], cfg.momentum, cfg.weight_decay, cfg.milestones, 0.1, cfg.steps_per_epoch)
