@@ -52,7 +52,7 @@ def main():
     pipe = pst.Pipeline(net, flat, ppv, case["B"], case["lr"], case.get("lr_np", case["lr"][-1]),
                         momentum=case.get("mom", 0.9), weight_decay=case.get("wd", 1e-4),
                         milestones=case.get("milestones", ()), steps_per_epoch=case.get("spe", 1 << 62),
-                        devices=devices, rank=rank, nccl_id=nid)
+                        devices=devices, rank=rank, nccl_id=nid, dropout_seed=case.get("dropout_seed", 0))
     if case.get("n_p") is not None:
         pipe.set_hybrid(case["n_p"] // case["spe"])
     for x, y in data:

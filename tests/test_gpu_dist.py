@@ -83,7 +83,8 @@ def _local(gpu, case, net, flat, data):
     ppv = tuple(case["ppv"])
     pipe = gpu.Pipeline(net, flat, ppv, case["B"], case["lr"], case.get("lr_np", case["lr"][-1]),
                         momentum=case.get("mom", 0.9), weight_decay=case.get("wd", 1e-4),
-                        milestones=case.get("milestones", ()), steps_per_epoch=case.get("spe", 1 << 62))
+                        milestones=case.get("milestones", ()), steps_per_epoch=case.get("spe", 1 << 62),
+                        dropout_seed=case.get("dropout_seed", 0))
     if case.get("n_p") is not None:
         pipe.set_hybrid(case["n_p"] // case["spe"])
     for x, y in data:
@@ -102,9 +103,12 @@ def _check(gpu, case, tag):
     data = W.batches(net.in_shape, case["B"], case["N"], seed=case["seed"] + 100)
     hp = hparams(case["lr"], K, case.get("lr_np", case["lr"][-1]), case.get("mom", 0.9), case.get("wd", 1e-4),
                  case.get("milestones", ()), 0.1, case.get("spe", 1 << 62))
-    ref = oracle_run(net, flat, ppv, data, hp, n_p=case.get("n_p"))
-    sp_p = oracle_spreads(net, ppv, ref, oracle_run(net, perturbed(flat), ppv, data, hp, n_p=case.get("n_p")))
-    sp_e = oracle_spreads(net, ppv, ref, oracle_run(net, flat, ppv, data, hp, n_p=case.get("n_p"), emu=True))
+    ds = case.get("dropout_seed", 0)
+    ref = oracle_run(net, flat, ppv, data, hp, n_p=case.get("n_p"), dropout_seed=ds)
+    sp_p = oracle_spreads(net, ppv, ref, oracle_run(net, perturbed(flat), ppv, data, hp, n_p=case.get("n_p"),
+                                                      dropout_seed=ds))
+    sp_e = oracle_spreads(net, ppv, ref, oracle_run(net, flat, ppv, data, hp, n_p=case.get("n_p"), emu=True,
+                                                      dropout_seed=ds))
     sp = allowances(sp_p, sp_e)
     got, work = _launch(case)
     for s in range(K):
@@ -163,3 +167,10 @@ def test_dist_k3_midblock(gpu):
     _check(gpu, dict(net="tiny_resnet", net_kw=dict(width=16, hw=8, n=2), ppv=[2, 6], B=32, N=9, seed=27,
                      lr=[0.002, 0.005, 0.01], lr_np=0.008, n_p=4, spe=2, milestones=[3], deep=True),
            "dist_k3_midblock_hybrid")
+
+
+def test_dist_k2_dropout(gpu):
+    """Dropout across processes: each rank's stage draws its masks from the shared counter-based
+    generator with its own forward counter (pst.h pst_layer.dropout, reading AMB-16b)."""
+    _check(gpu, dict(net="tiny_cnn", net_kw=dict(hw=8, dropout=0.4), ppv=[1], B=32, N=9, seed=29, lr=[0.05] * 2,
+                     wd=5e-4, dropout_seed=777), "dist_k2_dropout")

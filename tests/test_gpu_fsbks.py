@@ -68,3 +68,10 @@ def test_fsbks_rejects_hybrid_and_dist(pst):
     with pytest.raises(pst.PstError) as e:
         pst.Pipeline(net, flat, (2,), 8, [0.1, 0.1], 0.1, mapping=1, rank=0, nccl_id=pst.nccl_unique_id())
     assert e.value.code in (-6, -1)
+
+
+def test_fsbks_dropout(pst):
+    """Dropout under the FS/BKS mapping: the forward objects draw the masks, the backward objects
+    receive the post-dropout activations with the saved state."""
+    run_both(pst, W.tiny_cnn(hw=8, dropout=0.4), (1, 2), 32, 9, [0.05] * 3, wd=5e-4, per_step=False,
+             solver_kw=FSBKS, dropout_seed=4242).assert_ok()
