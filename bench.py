@@ -259,6 +259,13 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     cfg = W.CONFIGS[args.config]
     K = world
     if K in cfg.ppv:
@@ -332,7 +339,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
-    launches = pipe.launches() - l0
+    launches = int(sum_over_ranks(pipe.launches() - l0))   # every rank's kernels in the timed region
     clk = clocks.stop()
     value = args.steps * B / (ms / 1e3)
 
