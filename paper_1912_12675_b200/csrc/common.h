@@ -132,6 +132,9 @@ int pst_knob(const char* name, int dflt);
 // drains.  Kernels call pdl_wait() before their first global-memory access (read or write) and
 // pdl_trigger() right after it, so kernel N starts only once kernel N-1 has passed its own wait,
 // i.e. every kernel before N-1 is complete.  PST_PDL=0 disables the attribute (A/B timing).
+// Exception: the kernels that write weight shadows (sgd_kernel, conv_w_shadow_kernel) never call
+// pdl_trigger, so their dependents start only once they are complete; conv_ts_kernel relies on it
+// to load a layer's weights before its pdl_wait.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();

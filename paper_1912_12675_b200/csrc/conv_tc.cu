@@ -1013,7 +1013,8 @@ void conv_tc(const ConvSpec& c, cudaStream_t st) {
   PST_CHECK_ARG(c.S == 1 || c.S == 2, "conv stride must be 1 or 2");
   PST_CHECK_ARG((reinterpret_cast<uintptr_t>(c.in) & 15) == 0, "conv input must be 16B aligned");
   if (conv_ts(c, st)) return;
-  PST_CHECK_ARG(!c.bfuse, "fused bwd_pre needs the TS conv kernel");   // activation operand in TMEM (conv_ts.cu) where the tiling fits
+  PST_CHECK_ARG(!c.pre, "the band pre-pass needs the TS conv kernel");
+  PST_CHECK_ARG(!c.bfuse,"fused bwd_pre needs the TS conv kernel");   // activation operand in TMEM (conv_ts.cu) where the tiling fits
   FwdArgs a{};
   a.N = c.N; a.Ho = c.Ho; a.Wo = c.Wo;
   pixel_tile(c.N, c.Ho, c.Wo, 128, a.bimg, a.bh, a.bw);

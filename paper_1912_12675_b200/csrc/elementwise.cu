@@ -476,8 +476,8 @@ __device__ __forceinline__ int64_t shb_idx(int tap, int co, int ci, int Coutp, i
 
 template <bool kUpdate>
 __global__ void sgd_kernel(const SgdSpec s) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_wait();      // no early pdl_trigger: the next kernels may read the weights before their pdl_wait
+
   __shared__ float lr_sh;
   __shared__ int seg_sh;
   __shared__ int last_sh;
@@ -594,8 +594,8 @@ __global__ void wgrad_sum_kernel(const SgdSpec s) {
 
 __global__ void conv_w_shadow_kernel(const float* w, int cout, int cin, int k, int Coutp, int Cinp, act_t* sf,
                                      act_t* sb) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_wait();      // writes weight shadows: no early pdl_trigger (sgd_kernel)
+
   const int64_t n = (int64_t)cout * cin * k * k;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int kk = k * k;

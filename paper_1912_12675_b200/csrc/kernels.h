@@ -42,6 +42,26 @@ struct ConvSpec {
   int bfuse, brelu, bbn;
   float bscale;             // fused bwd_pre: dropout scale of the lower layer where z > 0 (0 = 1)
   unsigned long long* dbg;  // optional device timeline buffer [8][256] (CTA 0), debug only
+  // Band pre-pass (TS kernel only): the per-element BatchNorm step that produces this conv's
+  // input is done on the input band in shared memory after its TMA load, before the taps read it,
+  // instead of by a separate kernel; the transformed tensor is also written to `pre_out` for the
+  // tile's own input rows (every element exactly once), for the consumers that need it later.
+  //   pre 1 (forward, BN apply of the producing layer): `in` is that layer's conv output y;
+  //         x = relu?( gamma*(y-mean)*invstd + beta [+ pre_res] ), mean/invstd from pre_stats
+  //         (sum, sumsq over M values); CTA 0 writes pre_saved = (mean, invstd) and the running stats.
+  //   pre 2 (dgrad, BN backward of this layer): `in` is the pre-activation gradient gpre;
+  //         gy = gamma*invstd*(gpre - S1/M - xhat*S2/M), xhat = (pre_y - mean)*invstd,
+  //         (mean, invstd) = pre_saved, (S1, S2) = pre_stats.
+  // Positions outside the image are zero after the transform (the conv's zero padding).
+  int pre, pre_relu, pre_C;
+  const act_t* pre_res;     // pre 1: identity shortcut of the producer's block (shape of `in`) or null
+  const act_t* pre_y;       // pre 2: this layer's BN input y
+  const double* pre_stats;
+  const float* pre_gamma; const float* pre_beta;
+  float* pre_saved;
+  float* pre_run_mean; float* pre_run_var;
+  float pre_momentum, pre_eps;
+  act_t* pre_out;
 };
 void conv_tc(const ConvSpec& c, cudaStream_t st);
 // TS-mode variant (A operand in tensor memory, 3xTF32 build); returns false if the shape

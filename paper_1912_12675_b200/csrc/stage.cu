@@ -251,6 +251,8 @@ Stage::Stage(const NetInfo& net, int s_, int K_, int l0_, int l1_, int device, c
   sgd_.inv_power = hp.inv_power;
   build_shadows(sgd_, stream);
   PST_CUDA(cudaStreamSynchronize(stream));
+  for (int l = l0, b = 0; l < l1; ++l) bn_idx_.push_back(net.layers[l].spec.bn ? b++ : -1);
+  plan_fusion();
 }
 
 Stage::~Stage() {
@@ -309,66 +311,125 @@ size_t Stage::stage_x_bytes() const {
 }
 
 // ------------------------------------------------------------------ forward
+ConvSpec Stage::fwd_spec(int l, int64_t mb) const {
+  const int slot = (int)(mb % R);
+  const LayerInfo& li = net_.layers[l];
+  const LayerBufs& b = L_[l - l0];
+  const bool last_net = (l == (int)net_.layers.size() - 1);
+  ConvSpec c{};
+  c.in = in_tensor(l, mb);
+  c.N = batch_;
+  c.H = li.in_H;
+  c.W = li.in_W;
+  c.Cinp = li.Cinp;
+  c.Ho = li.Ho; c.Wo = li.Wo; c.Coutp = li.Coutp; c.Cout = li.spec.cout;
+  c.k = li.kk;
+  c.S = li.S;
+  c.off = -li.pad;
+  c.sgn = 1;
+  c.wshadow = b.sh_fwd;
+  c.relu = li.spec.relu;
+  c.bias = li.spec.bias ? w_ + (li.off_b - p_base) : nullptr;
+  if (li.spec.bn) {
+    c.epi = EPI_BN_STATS;
+    c.out = b.y[slot];
+    c.stats = b.stats;
+    c.relu = 0;
+  } else if (last_net) {
+    c.epi = EPI_BIAS_F32;
+    c.out = b.zf[slot];
+  } else {
+    c.epi = EPI_BIAS_ACT;
+    c.out = b.z[slot];
+  }
+  return c;
+}
+
+BnApplySpec Stage::bn_spec(int l, int64_t mb) const {
+  const int slot = (int)(mb % R);
+  const LayerInfo& li = net_.layers[l];
+  const LayerBufs& b = L_[l - l0];
+  const int bl = bn_idx_[l - l0];
+  BnApplySpec a{};
+  a.y = b.y[slot]; a.z = b.z[slot];
+  a.N = batch_; a.H = li.Ho; a.W = li.Wo; a.Cp = li.Coutp; a.C = li.spec.cout;
+  a.stats = b.stats;
+  a.gamma = w_ + (li.off_g - p_base);
+  a.beta = w_ + (li.off_be - p_base);
+  a.saved = b.saved[slot];
+  a.run_mean = run_ + run_off_[bl];
+  a.run_var = run_ + run_off_[bl] + li.Coutp;
+  a.momentum = 0.1f; a.eps = 1e-5f;
+  a.relu = li.spec.relu;
+  if (li.spec.residual) {
+    const LayerInfo& src = net_.layers[li.block_src];
+    a.res = li.block_src < l0 ? xin2_[mb % Rin] : in_tensor(li.block_src, mb);   // mid-block: received
+    a.res_mode = li.res_mode;
+    a.res_H = src.in_H; a.res_W = src.in_W; a.res_C = src.in_Cp; a.res_Creal = src.in_C;
+    a.res_pad = li.res_pad;
+  }
+  return a;
+}
+
+// The forward conv c of layer l+1 takes the BN apply of layer l: it reads l's conv output y and
+// writes l's z (kernels.h ConvSpec.pre 1).
+void Stage::set_pre_bn_apply(ConvSpec& c, int l, int64_t mb) const {
+  const BnApplySpec a = bn_spec(l, mb);
+  c.in = a.y;
+  c.pre = 1;
+  c.pre_relu = a.relu;
+  c.pre_C = a.C;
+  c.pre_res = a.res_mode == 1 ? a.res : nullptr;
+  c.pre_stats = a.stats;
+  c.pre_gamma = a.gamma; c.pre_beta = a.beta;
+  c.pre_saved = a.saved;
+  c.pre_run_mean = a.run_mean; c.pre_run_var = a.run_var;
+  c.pre_momentum = a.momentum; c.pre_eps = a.eps;
+  c.pre_out = a.z;
+}
+
+void Stage::plan_fusion() {
+  static const bool on = pst_knob("PST_FUSE_BN", 0) != 0;
+  fuse_fwd_.assign(l1 - l0, 0);
+  fuse_bwd_.assign(l1 - l0, 0);
+  if (!on) return;
+  for (int l = l0 + 1; l < l1; ++l) {
+    const LayerInfo& p = net_.layers[l - 1];
+    if (!p.spec.bn || p.spec.pool != 0 || p.spec.dropout > 0.f) continue;
+    if (p.spec.residual && p.res_mode != 1) continue;
+    ConvSpec c = fwd_spec(l, 0);
+    set_pre_bn_apply(c, l - 1, 0);
+    if (c.Cinp != p.Coutp || c.H != p.Ho || c.W != p.Wo) continue;
+    fuse_fwd_[l - l0] = conv_ts_fits(c) ? 1 : 0;
+  }
+  for (int l = l0; l < l1; ++l) {
+    const LayerInfo& li = net_.layers[l];
+    const LayerBufs& b = L_[l - l0];
+    if (!li.spec.bn || li.S != 1 || b.gin == nullptr) continue;
+    ConvSpec c{};
+    c.in = b.gpre; c.N = batch_; c.H = li.Ho; c.W = li.Wo; c.Cinp = li.Coutp;
+    c.Ho = li.in_H; c.Wo = li.in_W; c.Coutp = li.Cinp; c.Cout = li.in_C;
+    c.k = li.kk; c.S = 1; c.off = li.pad; c.sgn = -1; c.wshadow = b.sh_bwd; c.epi = EPI_DGRAD; c.out = b.gin;
+    c.pre = 2; c.pre_y = b.y[0]; c.pre_out = b.gy;
+    fuse_bwd_[l - l0] = conv_ts_fits(c) ? 1 : 0;
+  }
+}
+
 void Stage::enqueue_forward(int64_t mb, cudaStream_t st) {
   const int B = batch_;
   const int slot = (int)(mb % R);
   if (fwd_arena_n_) PST_CUDA(cudaMemsetAsync(fwd_arena_, 0, fwd_arena_n_ * sizeof(double), st));
   if (is_first())
     input_to_act(xstage_, xin_[mb % Rin], B, net_.in_C, net_.in_H, net_.in_W, net_.in_Cp, st);
-  int bn_local = 0;
   for (int l = l0; l < l1; ++l) {
     const LayerInfo& li = net_.layers[l];
     LayerBufs& b = L_[l - l0];
     const bool last_net = (l == (int)net_.layers.size() - 1);
-    ConvSpec c{};
-    c.in = in_tensor(l, mb);
-    c.N = B;
-    c.H = li.in_H;
-    c.W = li.in_W;
-    c.Cinp = li.Cinp;
-    c.Ho = li.Ho; c.Wo = li.Wo; c.Coutp = li.Coutp; c.Cout = li.spec.cout;
-    c.k = li.kk;
-    c.S = li.S;
-    c.off = -li.pad;
-    c.sgn = 1;
-    c.wshadow = b.sh_fwd;
-    c.relu = li.spec.relu;
-    c.bias = li.spec.bias ? w_ + (li.off_b - p_base) : nullptr;
-    if (li.spec.bn) {
-      c.epi = EPI_BN_STATS;
-      c.out = b.y[slot];
-      c.stats = b.stats;
-      c.relu = 0;
-    } else if (last_net) {
-      c.epi = EPI_BIAS_F32;
-      c.out = b.zf[slot];
-    } else {
-      c.epi = EPI_BIAS_ACT;
-      c.out = b.z[slot];
-    }
+    ConvSpec c = fwd_spec(l, mb);
+    if (fuse_fwd_[l - l0]) set_pre_bn_apply(c, l - 1, mb);   // BN apply of layer l-1 on the band
     if (!skip("fwd")) conv_tc(c, st);
-    if (li.spec.bn) {
-      BnApplySpec a{};
-      a.y = b.y[slot]; a.z = b.z[slot];
-      a.N = B; a.H = li.Ho; a.W = li.Wo; a.Cp = li.Coutp; a.C = li.spec.cout;
-      a.stats = b.stats;
-      a.gamma = w_ + (li.off_g - p_base);
-      a.beta = w_ + (li.off_be - p_base);
-      a.saved = b.saved[slot];
-      a.run_mean = run_ + run_off_[bn_local];
-      a.run_var = run_ + run_off_[bn_local] + li.Coutp;
-      a.momentum = 0.1f; a.eps = 1e-5f;
-      a.relu = li.spec.relu;
-      if (li.spec.residual) {
-        const LayerInfo& src = net_.layers[li.block_src];
-        a.res = li.block_src < l0 ? xin2_[mb % Rin] : in_tensor(li.block_src, mb);   // mid-block: received
-        a.res_mode = li.res_mode;
-        a.res_H = src.in_H; a.res_W = src.in_W; a.res_C = src.in_Cp; a.res_Creal = src.in_C;
-        a.res_pad = li.res_pad;
-      }
-      if (!skip("bnapply")) bn_apply(a, st);
-      ++bn_local;
-    }
+    const bool next_takes_bn = l + 1 < l1 && fuse_fwd_[l + 1 - l0];
+    if (li.spec.bn && !next_takes_bn && !skip("bnapply")) bn_apply(bn_spec(l, mb), st);
     if (li.spec.dropout > 0.f)   // after the ReLU, before the pool (pst.h pst_layer.dropout)
       dropout_fwd(b.z[slot], B, li.Ho, li.Wo, li.Coutp, li.spec.cout, dseed_, l, drop_thresh(li.spec.dropout),
                   drop_scale(li.spec.dropout), d_fmb_, st);
@@ -415,30 +476,34 @@ void Stage::enqueue_backward(int64_t mb, int dpar, cudaStream_t st) {
     pr.N = B; pr.H = li.Ho; pr.W = li.Wo; pr.Cp = li.Coutp; pr.C = li.spec.cout;
     pr.sums = b.sums;
     if (!skip("bwdpre") && !pre_done[l - l0]) bwd_pre(pr, st);
+    const bool fb = fuse_bwd_[l - l0] != 0;   // the dgrad does this layer's BN backward on its band
     const act_t* dY = b.gpre;
     if (li.spec.bn) {
-      BnBwdSpec bb{};
-      bb.gpre = b.gpre; bb.y = b.y[slot]; bb.saved = b.saved[slot]; bb.sums = b.sums;
-      bb.gamma = w_ + (li.off_g - p_base);  // current gamma (no stash)
-      bb.gy = b.gy;
-      bb.N = B; bb.H = li.Ho; bb.W = li.Wo; bb.Cp = li.Coutp; bb.C = li.spec.cout;
-      if (!skip("bnbwd")) bn_bwd_apply(bb, st);
+      if (!fb) {
+        BnBwdSpec bb{};
+        bb.gpre = b.gpre; bb.y = b.y[slot]; bb.saved = b.saved[slot]; bb.sums = b.sums;
+        bb.gamma = w_ + (li.off_g - p_base);  // current gamma (no stash)
+        bb.gy = b.gy;
+        bb.N = B; bb.H = li.Ho; bb.W = li.Wo; bb.Cp = li.Coutp; bb.C = li.spec.cout;
+        if (!skip("bnbwd")) bn_bwd_apply(bb, st);
+      }
       dY = b.gy;
     }
     // weight gradient from the saved input of this mini-batch
-    WgradSpec wg{};
-    wg.x = in_tensor(l, mb);
-    wg.N = B;
-    wg.H = li.in_H;
-    wg.W = li.in_W;
-    wg.Cinp = li.Cinp;
-    wg.dy = dY; wg.Ho = li.Ho; wg.Wo = li.Wo; wg.Coutp = li.Coutp;
-    wg.k = li.kk;
-    wg.S = li.S;
-    wg.pad = li.pad;
-    wg.part = b.wpart;
-    wg.ksplit = b.ksplit;
-    if (!skip("wgrad")) {
+    auto wgrad = [&]() {
+      WgradSpec wg{};
+      wg.x = in_tensor(l, mb);
+      wg.N = B;
+      wg.H = li.in_H;
+      wg.W = li.in_W;
+      wg.Cinp = li.Cinp;
+      wg.dy = dY; wg.Ho = li.Ho; wg.Wo = li.Wo; wg.Coutp = li.Coutp;
+      wg.k = li.kk;
+      wg.S = li.S;
+      wg.pad = li.pad;
+      wg.part = b.wpart;
+      wg.ksplit = b.ksplit;
+      if (skip("wgrad")) return;
       if (side_wgrad()) {
         PST_CUDA(cudaEventRecord(ev_fork, st));
         PST_CUDA(cudaStreamWaitEvent(wstream, ev_fork, 0));
@@ -449,9 +514,9 @@ void Stage::enqueue_backward(int64_t mb, int dpar, cudaStream_t st) {
       } else {
         conv_wgrad_tc(wg, st);
       }
-    }
+    };
     // input gradient with the CURRENT weights
-    if (b.gin != nullptr) {
+    auto dgrad = [&]() {
       ConvSpec c{};
       const act_t* src = dY;
       int sH = li.Ho, sW = li.Wo;
@@ -472,6 +537,16 @@ void Stage::enqueue_backward(int64_t mb, int dpar, cudaStream_t st) {
       c.wshadow = b.sh_bwd;
       c.epi = EPI_DGRAD;
       c.out = b.gin;
+      if (fb) {   // BN backward of this layer on the band: gpre (+ y) in, gy written for the wgrad
+        c.in = b.gpre;
+        c.pre = 2;
+        c.pre_C = li.spec.cout;
+        c.pre_y = b.y[slot];
+        c.pre_saved = b.saved[slot];
+        c.pre_stats = b.sums;
+        c.pre_gamma = w_ + (li.off_g - p_base);   // current gamma (no stash)
+        c.pre_out = b.gy;
+      }
       // fuse bwd_pre of layer l-1 (ReLU mask + BN backward sums) into this epilogue when layer
       // l-1 has no pooling and the TS kernel takes the shape
       if (fuse_on && l - 1 >= l0 && net_.layers[l - 1].spec.pool == 0 && conv_ts_fits(c)) {
@@ -497,6 +572,13 @@ void Stage::enqueue_backward(int64_t mb, int dpar, cudaStream_t st) {
       static const int dg_ctas = pst_knob("PST_DG_CTAS", 0);
       c.max_ctas = side_wgrad() ? dg_ctas : 0;
       if (!skip("dgrad")) conv_tc(c, st);
+    };
+    if (fb) {
+      dgrad();
+      wgrad();
+    } else {
+      wgrad();
+      if (b.gin != nullptr) dgrad();
     }
   }
   if (side_wgrad()) {

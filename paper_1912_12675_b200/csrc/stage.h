@@ -105,6 +105,16 @@ class Stage {
   act_t* in_tensor(int l, int64_t mb) const;     // input of layer l for mini-batch mb
   act_t* out_tensor(int l, int slot) const;      // saved output of layer l in ring slot `slot`
 
+  ConvSpec fwd_spec(int l, int64_t mb) const;                 // forward conv of layer l (no pre-pass)
+  BnApplySpec bn_spec(int l, int64_t mb) const;               // BN apply of layer l (bn layers)
+  void set_pre_bn_apply(ConvSpec& c, int l, int64_t mb) const;   // c (layer l+1) takes l's BN apply
+  void plan_fusion();
+  // Band pre-pass fusion (kernels.h ConvSpec.pre): fuse_fwd_[i] -- the forward conv of layer l0+i
+  // does the BN apply of layer l0+i-1; fuse_bwd_[i] -- the dgrad of layer l0+i does its own BN
+  // backward (its wgrad then forks after the dgrad, which writes gy).
+  std::vector<char> fuse_fwd_, fuse_bwd_;
+  std::vector<int> bn_idx_;                      // local BN index of each layer (run_off_), -1 if none
+
   std::vector<LayerBufs> L_;
   std::vector<act_t*> xin_;
   act_t* dbuf_[2] = {nullptr, nullptr};
