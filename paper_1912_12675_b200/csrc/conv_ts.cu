@@ -240,7 +240,7 @@ __device__ __forceinline__ void pre_pass(const TsArgs& a, const float* coef, uin
 template <int KC, int EPI, int TPS, int PRE, int SS>
 __global__ void __launch_bounds__(kTsThreads + PRE * 128, 1)
     conv_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
-                   const __grid_constant__ CUtensorMap tmB, const TsArgs a) {
+                   const __grid_constant__ CUtensorMap tmB, const __grid_constant__ TsArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   // [weights hi | weights lo] [band ring] [stats scratch 4 x 32 x 17 f32] [barriers] [tmem ptr]
   uint8_t* wsm = smem;
@@ -278,18 +278,15 @@ __global__ void __launch_bounds__(kTsThreads + PRE * 128, 1)
     ptx::mbar_init(wbar, 1);
     ptx::fence_mbar_init();
   }
+  if (threadIdx.x == 0) TSL(7, 1);   // barriers initialised
   if (warp == 1) ptx::tmem_alloc(tmem_ptr, 512);
-#pragma unroll 1
-  for (int t = threadIdx.x; t < 49; t += blockDim.x) {
-    int v = 0;
-#pragma unroll
-    for (int j = 0; j < 49; ++j) v = (j == t) ? a.tapshift[j] : v;
-    tsh[t] = v;
-  }
+  if (threadIdx.x == 32) TSL(7, 2);  // TMEM allocated
+  if (threadIdx.x < 49) tsh[threadIdx.x] = a.tapshift[threadIdx.x];   // __grid_constant__: read in place
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
+  if (threadIdx.x == 0) TSL(7, 3);   // past the prologue barrier
   // The weight shadows are written only by the update kernels (sgd_kernel, build_shadows), which do
   // not release their dependents early (common.h pdl_trigger), and at least one kernel separates
   // them from any conv; so the layer's weights load before pdl_wait, overlapping the previous
@@ -312,50 +309,50 @@ __global__ void __launch_bounds__(kTsThreads + PRE * 128, 1)
   __syncwarp();
   pdl_wait();      // no activation / statistics access above this line
   pdl_trigger();
+  if (threadIdx.x == 0) TSL(7, 4);   // past griddepcontrol.wait
   const uint32_t a_col0 = a.n_acc * a.accw;          // accumulators: columns [0, n_acc accw)
+  // band stage bs <- tile m, channel chunk kcc (elected producer lane)
+  auto issue_band = [&](int bs, int m, int kcc) {
+    const int n0 = a.nb > 1 ? m * a.nb : m / a.tpi;
+    const int y0 = a.nb > 1 ? 0 : (m % a.tpi) * a.rows_t;
+    if (KNOB(32)) { ptx::mbar_arrive(&full[bs]); return; }
+    if (SS) {   // three dense column-shifted bands (dx = lo .. lo+2), zero-filled outside the image
+      ptx::mbar_expect_tx(&full[bs], 3 * a.band_tx);
+#pragma unroll
+      for (int bx = 0; bx < 3; ++bx)
+        ptx::tma_load_4d(bands + bs * a.band_bytes + bx * 2 * a.ss_band, &tmA, &full[bs], (a.lo + bx) * kEPC,
+                         y0 + a.lo, n0, kcc * (KC / kEPC));
+      return;
+    }
+    ptx::mbar_expect_tx(&full[bs], a.pre2 ? 2 * a.band_tx : a.band_tx);
+    ptx::tma_load_4d(bands + bs * a.band_bytes, &tmA, &full[bs], a.lo * kEPC, y0 * a.S + a.lo, n0, kcc * (KC / kEPC));
+    if (a.pre2)
+      ptx::tma_load_4d(bands + bs * a.band_bytes + a.band2_off, &tmB, &full[bs], a.lo * kEPC, y0 * a.S + a.lo, n0,
+                       kcc * (KC / kEPC));
+  };
+  // the first band right after the dependency wait, before the role dispatch (the producer loop's
+  // code is cold at this point: issuing from here saves ~1 kcycle of the first tile's latency)
+#ifndef PST_NO_EARLY_BAND
+  if (warp == 0 && m0 < a.n_mtiles && !KNOB(16) && ptx::elect_one()) issue_band(0, m0, 0);
+#endif
+  __syncwarp();
 
   if (KNOB(16)) {
     // experiment: prologue and teardown only
   } else if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
-    if (false) {
-      if (a.stack) {  // (BN*EPC, hi/lo, planes, taps) -> smem [tap][plane][hi BN rows | lo BN rows]
-        ptx::tma_load_4d(wsm, &tmW, wbar, nt * a.BN * kEPC, 0, 0, 0);
-      } else if (a.w3d) {   // long rows: (BN*EPC, planes, taps)
-        ptx::tma_load_3d(wsm, &tmW, wbar, nt * a.BN * kEPC, 0, 0);                 // hi: taps [0, taps)
-        ptx::tma_load_3d(wsm + a.w_bytes, &tmW, wbar, nt * a.BN * kEPC, 0, a.taps);  // lo: taps [taps, 2 taps)
-      } else {
-        ptx::tma_load_4d(wsm, &tmW, wbar, 0, nt * a.BN, 0, 0);
-        ptx::tma_load_4d(wsm + a.w_bytes, &tmW, wbar, 0, nt * a.BN, 0, a.taps);
-      }
-    }
     __syncwarp();
     int bs = 0;
     uint32_t bph = 0;
     for (int m = m0; m < a.n_mtiles; m += mstep) {
-      const int n0 = a.nb > 1 ? m * a.nb : m / a.tpi;
-      const int y0 = a.nb > 1 ? 0 : (m % a.tpi) * a.rows_t;
       for (int kcc = 0; kcc < a.n_kc; ++kcc) {
         ptx::mbar_wait(&bempty[bs], bph ^ 1);
         if (lane == 0) TSL(0, dbg_i[0]++);
-        if (ptx::elect_one()) {
-          if (KNOB(32)) { ptx::mbar_arrive(&full[bs]); } else {
-          if (SS) {   // three dense column-shifted bands (dx = lo .. lo+2), zero-filled outside the image
-            ptx::mbar_expect_tx(&full[bs], 3 * a.band_tx);
-#pragma unroll
-            for (int bx = 0; bx < 3; ++bx)
-              ptx::tma_load_4d(bands + bs * a.band_bytes + bx * 2 * a.ss_band, &tmA, &full[bs], (a.lo + bx) * kEPC,
-                               y0 + a.lo, n0, kcc * (KC / kEPC));
-          } else {
-          ptx::mbar_expect_tx(&full[bs], a.pre2 ? 2 * a.band_tx : a.band_tx);
-          ptx::tma_load_4d(bands + bs * a.band_bytes, &tmA, &full[bs], a.lo * kEPC, y0 * a.S + a.lo, n0,
-                           kcc * (KC / kEPC));
-          }
-          if (a.pre2)
-            ptx::tma_load_4d(bands + bs * a.band_bytes + a.band2_off, &tmB, &full[bs], a.lo * kEPC,
-                             y0 * a.S + a.lo, n0, kcc * (KC / kEPC));
-          }
-        }
+#ifndef PST_NO_EARLY_BAND
+        if (!(m == m0 && kcc == 0) && ptx::elect_one()) issue_band(bs, m, kcc);   // the first: in the prologue
+#else
+        if (ptx::elect_one()) issue_band(bs, m, kcc);
+#endif
         __syncwarp();
         if (++bs == a.band_stages) { bs = 0; bph ^= 1; }
       }

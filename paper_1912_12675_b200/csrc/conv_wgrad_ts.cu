@@ -115,14 +115,22 @@ __global__ void __launch_bounds__(wt_threads(SETS), 1)
   const uint32_t tmem = *tmem_ptr;
   pdl_wait();      // no global memory access above this line
   pdl_trigger();
+  // stage sb <- unit (image group n0, row block y0): input band + dY box (elected producer lane)
+  auto issue_unit = [&](int sb, int n0, int y0) {
+    uint8_t* s0 = ring + sb * a.stage_bytes;
+    ptx::mbar_expect_tx(&full[sb], a.rawx_tx + a.rawd_bytes);
+    ptx::tma_load_4d(s0, &tmX, &full[sb], -a.pad * kEPC, y0 * a.S - a.pad, n0, pl0);
+    ptx::tma_load_4d(s0 + off_rawd, &tmD, &full[sb], 0, y0, n0, nt * (a.BNw / kEPC));
+  };
+  // the first unit right after the dependency wait, before the role dispatch (cold producer code)
+#ifndef PST_NO_EARLY_BAND
+  if (warp == 0 && n_iter > 0 && ptx::elect_one())
+    issue_unit(0, (u_lo / a.ny) * a.nb, (u_lo % a.ny) * a.bh);
+#endif
+  __syncwarp();
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
-    if (ptx::elect_one()) {
-      ptx::prefetch_tmap(&tmX);
-      ptx::prefetch_tmap(&tmD);
-    }
-    __syncwarp();
     int sb = 0;
     uint32_t sbph = 0;
     int uq = u_lo / a.ny, ur = u_lo % a.ny;   // unit -> (image group, row block), advanced incrementally
@@ -131,12 +139,11 @@ __global__ void __launch_bounds__(wt_threads(SETS), 1)
       if (++ur == a.ny) { ur = 0; ++uq; }
       ptx::mbar_wait(&empty[sb], sbph ^ 1);
       if (lane == 0) WTL(0, it);
-      if (ptx::elect_one()) {
-        uint8_t* s0 = ring + sb * a.stage_bytes;
-        ptx::mbar_expect_tx(&full[sb], a.rawx_tx + a.rawd_bytes);
-        ptx::tma_load_4d(s0, &tmX, &full[sb], -a.pad * kEPC, y0 * a.S - a.pad, n0, pl0);
-        ptx::tma_load_4d(s0 + off_rawd, &tmD, &full[sb], 0, y0, n0, nt * (a.BNw / kEPC));
-      }
+#ifndef PST_NO_EARLY_BAND
+      if (it > 0 && ptx::elect_one()) issue_unit(sb, n0, y0);
+#else
+      if (ptx::elect_one()) issue_unit(sb, n0, y0);
+#endif
       __syncwarp();
       if (++sb == a.SB) { sb = 0; sbph ^= 1; }
     }

@@ -76,6 +76,9 @@ int pst_op_conv2d_fwd(const float* x, const float* w, float* y, int N, int Cin, 
       std::vector<unsigned long long> h(8 * 256);
       PST_CUDA(cudaMemcpy(h.data(), c.dbg, h.size() * 8, cudaMemcpyDeviceToHost));
       const char* names[8] = {"prod_issue", "ev1", "ev2", "ev3", "ev4", "epi_start", "epi_done", "start"};
+      std::printf("TL prologue  barriers %.2f  tmem %.2f  sync %.2f  pdl_wait %.2f\n",
+                  (double)(long long)(h[7 * 256 + 1] - h[7 * 256]) / 1e3, (double)(long long)(h[7 * 256 + 2] - h[7 * 256]) / 1e3,
+                  (double)(long long)(h[7 * 256 + 3] - h[7 * 256]) / 1e3, (double)(long long)(h[7 * 256 + 4] - h[7 * 256]) / 1e3);
       for (int e = 0; e < 7; ++e) {
         std::printf("TL %-10s", names[e]);
         for (int i = 0; i < 40 && h[e * 256 + i]; ++i) std::printf(" %7.2f", (double)(long long)(h[e * 256 + i] - h[7 * 256]) / 1e3);
