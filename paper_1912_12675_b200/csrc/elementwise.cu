@@ -88,36 +88,35 @@ constexpr int kU = PST_KU;   // 16-byte vectors per thread per pass (plane-block
 __global__ void bn_apply_kernel(const BnApplySpec s) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float sc[2 * E];
+  // per-warp coefficients (lanes 0..E-1 compute, shuffles broadcast): no block-wide barrier
   const int plane = blockIdx.y;
   const int c0 = plane * E;
   const int npix = s.N * s.H * s.W;
   const double M = (double)npix;
-  if (threadIdx.x < E) {
-    const int c = c0 + threadIdx.x;
-    float scale = 0.f, shift = 0.f;
-    if (c < s.C) {
-      const double mean = s.stats[2 * c] / M;
-      double var = s.stats[2 * c + 1] / M - mean * mean;
-      var = var < 0.0 ? 0.0 : var;
-      const float invstd = (float)(1.0 / sqrt(var + (double)s.eps));
-      const float g = s.gamma[c], b = s.beta[c];
-      scale = g * invstd;
-      shift = b - (float)mean * g * invstd;
-      if (blockIdx.x == 0) {
-        s.saved[2 * c] = (float)mean;
-        s.saved[2 * c + 1] = invstd;
-        s.run_mean[c] = (1.f - s.momentum) * s.run_mean[c] + s.momentum * (float)mean;
-        s.run_var[c] = (1.f - s.momentum) * s.run_var[c] + s.momentum * (float)(var * M / (M - 1.0));
-      }
+  const int lane = threadIdx.x & 31;
+  float my_scale = 0.f, my_shift = 0.f;
+  if (lane < E && c0 + lane < s.C) {
+    const int c = c0 + lane;
+    const double mean = s.stats[2 * c] / M;
+    double var = s.stats[2 * c + 1] / M - mean * mean;
+    var = var < 0.0 ? 0.0 : var;
+    const float invstd = (float)(1.0 / sqrt(var + (double)s.eps));
+    const float g = s.gamma[c], b = s.beta[c];
+    my_scale = g * invstd;
+    my_shift = b - (float)mean * g * invstd;
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      s.saved[2 * c] = (float)mean;
+      s.saved[2 * c + 1] = invstd;
+      s.run_mean[c] = (1.f - s.momentum) * s.run_mean[c] + s.momentum * (float)mean;
+      s.run_var[c] = (1.f - s.momentum) * s.run_var[c] + s.momentum * (float)(var * M / (M - 1.0));
     }
-    sc[threadIdx.x] = scale;
-    sc[E + threadIdx.x] = shift;
   }
-  __syncthreads();
   float scale[E], shift[E];
 #pragma unroll
-  for (int j = 0; j < E; ++j) { scale[j] = sc[j]; shift[j] = sc[E + j]; }
+  for (int j = 0; j < E; ++j) {
+    scale[j] = __shfl_sync(0xffffffffu, my_scale, j);
+    shift[j] = __shfl_sync(0xffffffffu, my_shift, j);
+  }
   const act_t* yp = s.y + (size_t)plane * npix * E;
   act_t* zp = s.z + (size_t)plane * npix * E;
   const int rnpix = s.N * s.res_H * s.res_W;
@@ -358,29 +357,27 @@ __global__ void bwd_pre_kernel(const BwdPreSpec s) {
 __global__ void bn_bwd_apply_kernel(const BnBwdSpec s) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float co[5 * E];   // k1, m1, m2, mean, invstd of the plane's channels
+  // per-warp coefficients (k1, m1, m2, mean, invstd of the plane's channels; lanes 0..E-1, shuffles)
   const int plane = blockIdx.y;
   const int c0 = plane * E;
   const int npix = s.N * s.H * s.W;
   const double M = (double)npix;
-  if (threadIdx.x < E) {
-    const int c = c0 + threadIdx.x;
-    float k1 = 0.f, m1 = 0.f, m2 = 0.f, mu = 0.f, iv = 0.f;
-    if (c < s.C) {
-      mu = s.saved[2 * c];
-      iv = s.saved[2 * c + 1];
-      k1 = s.gamma[c] * iv;
-      m1 = (float)(s.sums[2 * c] / M);
-      m2 = (float)(s.sums[2 * c + 1] / M);
-    }
-    co[threadIdx.x] = k1; co[E + threadIdx.x] = m1; co[2 * E + threadIdx.x] = m2;
-    co[3 * E + threadIdx.x] = mu; co[4 * E + threadIdx.x] = iv;
+  const int lane = threadIdx.x & 31;
+  float mk1 = 0.f, mm1 = 0.f, mm2 = 0.f, mmu = 0.f, miv = 0.f;
+  if (lane < E && c0 + lane < s.C) {
+    const int c = c0 + lane;
+    mmu = s.saved[2 * c];
+    miv = s.saved[2 * c + 1];
+    mk1 = s.gamma[c] * miv;
+    mm1 = (float)(s.sums[2 * c] / M);
+    mm2 = (float)(s.sums[2 * c + 1] / M);
   }
-  __syncthreads();
   float k1[E], m1[E], m2[E], mu[E], iv[E];
 #pragma unroll
   for (int j = 0; j < E; ++j) {
-    k1[j] = co[j]; m1[j] = co[E + j]; m2[j] = co[2 * E + j]; mu[j] = co[3 * E + j]; iv[j] = co[4 * E + j];
+    k1[j] = __shfl_sync(0xffffffffu, mk1, j); m1[j] = __shfl_sync(0xffffffffu, mm1, j);
+    m2[j] = __shfl_sync(0xffffffffu, mm2, j); mu[j] = __shfl_sync(0xffffffffu, mmu, j);
+    iv[j] = __shfl_sync(0xffffffffu, miv, j);
   }
   const act_t* gp = s.gpre + (size_t)plane * npix * E;
   const act_t* yp = s.y + (size_t)plane * npix * E;
