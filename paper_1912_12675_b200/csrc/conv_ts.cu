@@ -267,16 +267,18 @@ __global__ void __launch_bounds__(kTsThreads + PRE * 128, 1)
   const int m0 = blockIdx.x / a.n_ntiles, mstep = gridDim.x / a.n_ntiles;
   const int planes_w = a.Cinp / kEPC;                // weight planes per tap
 
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < a.band_stages; ++i) {
-      ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&bempty[i], SS ? 1 : 4 * kTsSets);   // SS: released by the MMA commit
-      ptx::mbar_init(&ready[i], 4);
+  if (warp == 0) {   // lane i initialises the i-th barrier of each ring (the rings have <= 16 entries)
+    bool any = false;
+    if (lane < a.band_stages) {
+      ptx::mbar_init(&full[lane], 1);
+      ptx::mbar_init(&bempty[lane], SS ? 1 : 4 * kTsSets);   // SS: released by the MMA commit
+      ptx::mbar_init(&ready[lane], 4);
+      any = true;
     }
-    for (int i = 0; i < a.n_slots; ++i) { ptx::mbar_init(&afull[i], 4); ptx::mbar_init(&aempty[i], 1); }
-    for (int i = 0; i < a.n_acc; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 4); }
-    ptx::mbar_init(wbar, 1);
-    ptx::fence_mbar_init();
+    if (lane < a.n_slots) { ptx::mbar_init(&afull[lane], 4); ptx::mbar_init(&aempty[lane], 1); any = true; }
+    if (lane < a.n_acc) { ptx::mbar_init(&tfull[lane], 1); ptx::mbar_init(&tempty[lane], 4); any = true; }
+    if (lane == 0) { ptx::mbar_init(wbar, 1); any = true; }
+    if (any) ptx::fence_mbar_init();
   }
   if (threadIdx.x == 0) TSL(7, 1);   // barriers initialised
   if (warp == 1) ptx::tmem_alloc(tmem_ptr, 512);

@@ -93,11 +93,12 @@ __global__ void __launch_bounds__(wt_threads(SETS), 1)
   const uint32_t acc_cols = (uint32_t)a.G * a.BNw;       // accumulators: [0, G*BNw)
   const uint32_t slot_cols = (uint32_t)a.G * 2 * a.P16;  // per slot: G tiles x (P16 hi + P16 lo)
 
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < a.SB; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
-    for (int i = 0; i < a.St; ++i) { ptx::mbar_init(&ready[i], 4); ptx::mbar_init(&afree[i], 1); }
-    ptx::mbar_init(tfull, 1);
-    ptx::fence_mbar_init();
+  if (warp == 0) {   // lane i initialises the i-th barrier of each ring (<= 8 entries each)
+    bool any = false;
+    if (lane < a.SB) { ptx::mbar_init(&full[lane], 1); ptx::mbar_init(&empty[lane], 1); any = true; }
+    if (lane < a.St) { ptx::mbar_init(&ready[lane], 4); ptx::mbar_init(&afree[lane], 1); any = true; }
+    if (lane == 0) { ptx::mbar_init(tfull, 1); any = true; }
+    if (any) ptx::fence_mbar_init();
   }
   if (threadIdx.x < a.P16) {   // pixel table: float offset of pixel p in the band (-1: padding)
     const int p = threadIdx.x;
